@@ -1,0 +1,149 @@
+"""Seeded synthetic inputs for the five BASELINE.json configurations.
+
+There is no public dataset for this path; every input
+is a product A = G1 G2 of seeded random factors, exactly like the reference's
+``random_standardized`` generator (matrices.py:131-146: PCG64
+``default_rng(seed)``, left n x r drawn first, then right r x m, A = left @
+right).  Streams are keyed by their global index b, so a stream's bytes do not
+depend on how many GPUs share the batch.
+
+Host generators (numpy) feed the tests and the CPU oracle; ``device_*``
+generators (torch, on the GPU) feed bench.py at full size, and the sampled
+streams' exact bytes are copied back for the oracle spot check.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    streams: int
+    n: int
+    m: int
+    r: int          # construction rank (C3: upper end of U{4..32})
+    k: int
+    r_cap: int      # stored-rank capacity on the device
+
+
+CONFIGS = {
+    "c1": Config("c1", 1, 256, 256, 16, 1, 16),
+    "c2": Config("c2", 1, 4096, 1024, 64, 1, 64),
+    "c3": Config("c3", 4096, 512, 128, 32, 1, 32),
+    "c4": Config("c4", 1, 8192, 2048, 512, 1, 512),
+    "c5": Config("c5", 65536, 1024, 64, 16, 8, 16),
+}
+
+
+def random_standardized(n, m, r, seed):
+    """Restatement of matrices.random_standardized (matrices.py:131-146)."""
+    rng = np.random.default_rng(seed)
+    left = rng.standard_normal((n, r))
+    right = rng.standard_normal((r, m))
+    return left @ right
+
+
+def c1():
+    """Config 1: consistent system plus 1e-8 noise."""
+    A = random_standardized(256, 256, 16, 0)
+    g = np.random.default_rng(1)
+    x0 = g.standard_normal(256)
+    y = A @ x0 + 1e-8 * g.standard_normal(256)
+    return A, y
+
+
+def c2():
+    A = random_standardized(4096, 1024, 64, 0)
+    return A, np.random.default_rng(1).standard_normal(4096)
+
+
+def c4():
+    A = random_standardized(8192, 2048, 512, 0)
+    return A, np.random.default_rng(1).standard_normal(8192)
+
+
+def c3_stream(b, n=512, m=128):
+    """Stream b of config 3: r_b ~ U{4..32}; seeds keyed by (3, b, .)."""
+    r = int(np.random.default_rng(np.random.SeedSequence([3, b, 0])).integers(4, 33))
+    seed = int(np.random.SeedSequence([3, b, 1]).generate_state(1, np.uint64)[0])
+    A = random_standardized(n, m, r, seed)
+    y = np.random.default_rng(np.random.SeedSequence([3, b, 2])).standard_normal(n)
+    return A, y, r
+
+
+def c5_stream(b, n=1024, m=64, r=16, k=8):
+    """Stream b of config 5: even b Gaussian factors, odd b integer factors
+    uniform in {-3..3} (exact rank detection); k N(0,1) right-hand sides."""
+    rng = np.random.default_rng(np.random.SeedSequence([5, b]))
+    if b % 2 == 0:
+        g1 = rng.standard_normal((n, r))
+        g2 = rng.standard_normal((r, m))
+    else:
+        g1 = rng.integers(-3, 4, (n, r)).astype(np.float64)
+        g2 = rng.integers(-3, 4, (r, m)).astype(np.float64)
+    Y = rng.standard_normal((n, k))
+    return g1 @ g2, Y
+
+
+def host_batch(cfg_name, streams, n=None):
+    """rows[S, n, m], targets[S, n, k] for the listed global stream indices."""
+    cfg = CONFIGS[cfg_name]
+    n = n or cfg.n
+    rows, tg = [], []
+    for b in streams:
+        if cfg_name == "c5":
+            A, Y = c5_stream(b, cfg.n, cfg.m, cfg.r, cfg.k)
+        elif cfg_name == "c3":
+            A, y, _ = c3_stream(b, cfg.n, cfg.m)
+            Y = y[:, None]
+        else:
+            raise ValueError("host_batch covers the batched configs c3 and c5")
+        rows.append(A[:n]); tg.append(Y[:n])
+    return np.stack(rows), np.stack(tg)
+
+
+def device_batch(cfg_name, b0, b1, device, dtype=None, chunk=2048):
+    """Generate streams [b0, b1) of a batched config on the GPU (torch RNG,
+    seeded per chunk of ``chunk`` global stream indices so that a stream's
+    bytes are independent of the sharding).  Returns rows[S, n, m] and
+    targets[S, n, k] as float64 (or ``dtype``) device tensors."""
+    import torch
+
+    cfg = CONFIGS[cfg_name]
+    S = b1 - b0
+    rows = torch.empty((S, cfg.n, cfg.m), dtype=torch.float64, device=device)
+    tg = torch.empty((S, cfg.n, cfg.k), dtype=torch.float64, device=device)
+    gen = torch.Generator(device=device)
+    c0 = b0 - b0 % chunk
+    for cs in range(c0, b1, chunk):
+        gen.manual_seed(int(np.random.SeedSequence([int(cfg_name[1]), cs]).generate_state(1, np.uint64)[0] >> 1))
+        cnt = chunk
+        if cfg_name == "c5":
+            g1 = torch.randn((cnt, cfg.n, cfg.r), generator=gen, dtype=torch.float64, device=device)
+            g2 = torch.randn((cnt, cfg.r, cfg.m), generator=gen, dtype=torch.float64, device=device)
+            i1 = torch.randint(-3, 4, (cnt, cfg.n, cfg.r), generator=gen, device=device).to(torch.float64)
+            i2 = torch.randint(-3, 4, (cnt, cfg.r, cfg.m), generator=gen, device=device).to(torch.float64)
+            odd = (torch.arange(cs, cs + cnt, device=device) % 2 == 1).view(-1, 1, 1)
+            g1 = torch.where(odd, i1, g1)
+            g2 = torch.where(odd, i2, g2)
+            A = torch.bmm(g1, g2)
+            del g1, g2, i1, i2
+        else:  # c3: per-stream rank r_b ~ U{4..32}: zero the factor columns beyond r_b
+            rb = torch.randint(4, 33, (cnt,), generator=gen, device=device)
+            g1 = torch.randn((cnt, cfg.n, cfg.r), generator=gen, dtype=torch.float64, device=device)
+            g2 = torch.randn((cnt, cfg.r, cfg.m), generator=gen, dtype=torch.float64, device=device)
+            mask = (torch.arange(cfg.r, device=device).view(1, 1, -1) < rb.view(-1, 1, 1)).to(torch.float64)
+            A = torch.bmm(g1 * mask, g2)
+            del g1, g2
+        Y = torch.randn((cnt, cfg.n, cfg.k), generator=gen, dtype=torch.float64, device=device)
+        lo, hi = max(cs, b0), min(cs + cnt, b1)
+        rows[lo - b0:hi - b0] = A[lo - cs:hi - cs]
+        tg[lo - b0:hi - b0] = Y[lo - cs:hi - cs]
+        del A, Y
+    if dtype is not None and dtype != torch.float64:
+        rows, tg = rows.to(dtype), tg.to(dtype)
+    return rows, tg

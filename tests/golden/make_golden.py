@@ -1,0 +1,122 @@
+"""Generate the golden parity fixtures by running the REFERENCE itself.
+
+Run in the build container only (it imports rankrls from /root/reference,
+which does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture records the reference's own outputs on seeded inputs:
+per-row branch sequence (``RecursiveSolver.update().branch``, solver.py:231-250),
+final rank, the solution of ``solve_batch`` (the ``ingest`` fast path,
+solver.py:406-422; one call per right-hand side, since the reference has no
+multi-RHS API) and, where noted, ``pinv_from_scratch`` (tracking.py:128-142).
+The tests compare the C oracle and the CUDA path against these files.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", ".."))
+
+from rankrls import matrices, solver, tracking  # noqa: E402  (the reference)
+from rankrls.solver import EpsPolicy  # noqa: E402
+
+from paper_2106_11594_b200 import workloads  # noqa: E402  (input recipes only)
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def ref_stream(A, Y, variant="general", eps=None):
+    """Reference branch log (update fold, RHS 0) and per-RHS solve_batch."""
+    Y = np.asarray(Y, dtype=np.float64).reshape(A.shape[0], -1)
+    s = solver.RecursiveSolver(A.shape[1], variant=variant, eps=eps)
+    branch = np.array([s.update(row, t).branch == "independent" for row, t in zip(A, Y[:, 0])],
+                      dtype=np.uint8)
+    xs, rank = [], None
+    for c in range(Y.shape[1]):
+        x, rank = solver.solve_batch(A, Y[:, c], variant=variant, eps=eps)
+        xs.append(x)
+    return branch, np.stack(xs, axis=1), rank, s.solution.copy()
+
+
+def conditioned_stream(rng, n, m, r):
+    """Rank-r rows: r orthogonal rows scaled in [0.5, 2] then random
+    combinations of them (the construction of test_solver.py:12-27)."""
+    q, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    head = rng.uniform(0.5, 2.0, r)[:, None] * q.T
+    if n > r:
+        return np.vstack([head, rng.standard_normal((n - r, r)) @ head])
+    return head[:n]
+
+
+def main():
+    # -- config 1, full size: x, branches, rank and A+ -----------------------
+    A, y = workloads.c1()
+    branch, X, rank, x_fold = ref_stream(A, y)
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), A=A, y=y, branch=branch, x=X[:, 0],
+                        x_fold=x_fold, rank=rank, pinv=tracking.pinv_from_scratch(A))
+
+    # -- config 5 sample: 3 Gaussian + 3 integer streams, first 192 rows -----
+    streams = [0, 1, 2, 3, 4, 5]
+    rows, tg = workloads.host_batch("c5", streams, n=192)
+    br, xs, ranks = [], [], []
+    for i in range(len(streams)):
+        b_, X_, r_, _ = ref_stream(rows[i], tg[i])
+        br.append(b_); xs.append(X_); ranks.append(r_)
+    np.savez_compressed(os.path.join(OUT, "c5_sample.npz"), streams=np.array(streams),
+                        rows=rows, targets=tg, branch=np.stack(br), x=np.stack(xs),
+                        rank=np.array(ranks))
+
+    # -- config 3 sample: 2 streams, first 256 rows ---------------------------
+    streams = [0, 1]
+    rows, tg = workloads.host_batch("c3", streams, n=256)
+    br, xs, ranks = [], [], []
+    for i in range(len(streams)):
+        b_, X_, r_, _ = ref_stream(rows[i], tg[i])
+        br.append(b_); xs.append(X_); ranks.append(r_)
+    np.savez_compressed(os.path.join(OUT, "c3_sample.npz"), streams=np.array(streams),
+                        rows=rows, targets=tg, branch=np.stack(br), x=np.stack(xs),
+                        rank=np.array(ranks))
+
+    # -- all three variants on well-conditioned small streams, with A+ --------
+    rng = np.random.default_rng(2106)
+    cases = {}
+    for case in range(12):
+        n = int(rng.integers(1, 30)); m = int(rng.integers(1, 24))
+        r = int(rng.integers(1, min(n, m) + 1))
+        A = conditioned_stream(rng, n, m, r)
+        y = rng.standard_normal(n)
+        cases[f"A{case}"] = A; cases[f"y{case}"] = y
+        for v in solver.VARIANTS:
+            branch, X, rank, _ = ref_stream(A, y, variant=v)
+            cases[f"{v}_branch{case}"] = branch
+            cases[f"{v}_x{case}"] = X[:, 0]
+            cases[f"{v}_rank{case}"] = np.array(rank)
+            cases[f"{v}_pinv{case}"] = tracking.pinv_from_scratch(A, variant=v)
+    np.savez_compressed(os.path.join(OUT, "variants.npz"), **cases)
+
+    # -- Kahan(100, 0.2): the absolute clause of the rank test ---------------
+    # (test_stability_harness.py:32-45: fixed eps 1e-8 truncates to rank 99)
+    K, _ = matrices.kahan(100, 0.2)
+    s = solver.RecursiveSolver(100, eps=EpsPolicy.fixed(1e-8))
+    s.ingest(K, np.zeros(100))
+    np.savez_compressed(os.path.join(OUT, "kahan.npz"), K=K, rank_fixed=s.rank,
+                        rank_auto=solver.solve_batch(K, np.zeros(100))[1],
+                        pinv_auto=tracking.pinv_from_scratch(K))
+
+    # -- Pascal(10) in float64 (stability band anchor, test_acceptance.py:159-178)
+    P10 = matrices.pascal(10).astype(np.float64)
+    np.savez_compressed(os.path.join(OUT, "pascal10.npz"), P=P10,
+                        pinv=tracking.pinv_from_scratch(P10))
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
