@@ -1,0 +1,134 @@
+/*
+ * rgb.h -- C ABI of the B200-native rank-Greville recursive least-squares
+ * library (librgb.so).  arXiv 2106.11594, Algorithm 1.
+ *
+ * Plain C: raw device pointers, sizes and a cudaStream_t passed as void*.
+ * The caller owns every buffer (allocate with cudaMalloc, torch, cupy ...);
+ * the library allocates nothing and keeps no state between calls except a
+ * thread-local error string.  Every call is asynchronous on `stream`.
+ * Calls on one state must be stream-ordered (single writer, as SPEC.md:197);
+ * distinct states may run concurrently on different streams or GPUs.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/rankrls/<file>:<line>); INTEGRATION.md shows the
+ * ctypes binding a maintainer of the reference would add.
+ */
+#ifndef RGB_H_
+#define RGB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RGB_ABI_VERSION 1
+
+/* scalar kinds: scalars.py:141-147 (FLOAT64); FLOAT32 is a new kind */
+enum { RGB_F64 = 0, RGB_F32 = 1 };
+/* basis flavours: solver.py:29 VARIANTS */
+enum { RGB_GENERAL = 0, RGB_ORTHOGONAL = 1, RGB_ORTHONORMAL = 2 };
+/* EpsPolicy modes usable with floats: solver.py:32-72 ("exact" is rational-only) */
+enum { RGB_EPS_AUTO = 0, RGB_EPS_FIXED = 1 };
+
+/* return codes */
+enum {
+  RGB_OK = 0,
+  RGB_E_INVALID = -1,     /* bad argument: maps to ValueError (solver.py:142-158) */
+  RGB_E_UNSUPPORTED = -2, /* shape beyond kernel limits */
+  RGB_E_CUDA = -3         /* CUDA launch or runtime failure */
+};
+
+/* per-stream status bits (the stream is frozen once one is set) */
+enum {
+  RGB_ST_RANK_CAP = 1,  /* an independent row arrived with rank == r_cap */
+  RGB_ST_NONFINITE = 2, /* NaN/Inf row or target (scalars.py:122-123 raises) */
+  RGB_ST_BAD_ALPHA = 4  /* orthogonal rescaling factor zero (solver.py:364-365) */
+};
+
+/* Constructor arguments of RecursiveSolver (solver.py:140-141), batched:
+ * num_streams independent solvers of m regressors sharing one shape, each
+ * with k right-hand sides. */
+typedef struct rgb_config {
+  int64_t num_streams; /* B */
+  int32_t m;           /* num_regressors */
+  int32_t k;           /* right-hand sides per stream (reference: 1) */
+  int32_t r_cap;       /* stored-rank capacity; the reference grows unbounded */
+  int32_t dtype;       /* RGB_F64 / RGB_F32 */
+  int32_t variant;     /* RGB_GENERAL / RGB_ORTHOGONAL / RGB_ORTHONORMAL */
+  int32_t eps_mode;    /* RGB_EPS_AUTO / RGB_EPS_FIXED */
+  double eps_value;    /* EpsPolicy.fixed(value) */
+  double alpha;        /* orthogonal rescaling constant (solver.py:362) */
+} rgb_config;
+
+/* Solver state (solver.py:164-171), device pointers, row-major:
+ *   basis    [B][r_cap][m]      C       (solver._basis)
+ *   dual     [B][r_cap][m]      C~      (solver._dual; == basis for orthonormal)
+ *   gram_inv [B][r_cap][r_cap]  P^-1    (solver._gram_inv)
+ *   x        [B][k][m]          one solution per right-hand side (solver._x)
+ *   rank [B] int32, nobs [B] int64, status [B] int32
+ * Rows/columns beyond the current rank must be zero (rgb_state_reset). */
+typedef struct rgb_state {
+  void *basis;
+  void *dual;
+  void *gram_inv;
+  void *x;
+  int32_t *rank;
+  int64_t *nobs;
+  int32_t *status;
+} rgb_state;
+
+/* Optional per-row outputs of rgb_ingest; NULL members are not written. */
+typedef struct rgb_logs {
+  uint8_t *branch; /* [B][T]: 1 independent, 0 dependent (UpdateReport.branch, solver.py:84-91) */
+  void *coords;    /* [B][T][r_cap]: coordinate-factor row (_UpdateStep.coords_row, solver.py:94-109,
+                      the rows of B in A = B C, tracking.py:54-74), zero padded */
+  void *resid;     /* [B][T][k]: a-priori residual y - a.x (UpdateReport.predicted_residual) */
+  void *gain;      /* [B][m]: gain of the last ingested row (UpdateReport.gain) */
+} rgb_logs;
+
+/* Library ABI version (RGB_ABI_VERSION). */
+int rgb_abi_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *rgb_last_error(void);
+
+/* Empty solver state: RecursiveSolver.__init__ (solver.py:160-171) for all B
+ * streams -- zero factors and solutions, rank 0, nobs 0, status 0. */
+int rgb_state_reset(const rgb_config *cfg, rgb_state *state, void *stream);
+
+/* Fold T rows into every stream:
+ *   rows    : stream b's rows start at rows + b * rows_stride (elements),
+ *             T rows of m contiguous values (rows_stride 0 means T*m);
+ *   targets : stream b's targets at targets + b * targets_stride, T x k
+ *             (targets_stride 0 means T*k).
+ * Replaces RecursiveSolver.ingest (solver.py:252-319) and, with T = 1,
+ * RecursiveSolver.update (solver.py:231-250); solve_batch (solver.py:406-422)
+ * is reset + ingest.  Branch decisions use the reference's rank test
+ * (solver.py:292-296).  Streams whose status is nonzero are skipped. */
+int rgb_ingest(const rgb_config *cfg, rgb_state *state, const void *rows, int64_t rows_stride,
+               const void *targets, int64_t targets_stride, int64_t T, const rgb_logs *logs,
+               void *stream);
+
+/* RecursiveSolver.project + is_dependent (solver.py:210-229) for one row per
+ * stream: coords [B][r_cap] (zero padded), rejection [B][m], rej_sq [B],
+ * dependent [B] (uint8).  Any output pointer may be NULL. */
+int rgb_project(const rgb_config *cfg, const rgb_state *state, const void *rows, void *coords,
+                void *rejection, void *rej_sq, uint8_t *dependent, void *stream);
+
+/* Pseudoinverse from the factors (PseudoinverseTracker.pinv, tracking.py:19-85;
+ * closed form A+ = C~^T P^-1 B^T):
+ *   coords : [B][n][r_cap] coordinate-factor log written by rgb_ingest,
+ *   out    : [B][m][n].  Uses the current rank of each stream. */
+int rgb_pinv(const rgb_config *cfg, const rgb_state *state, const void *coords, int64_t n,
+             void *out, void *stream);
+
+/* Covariance V = A+ A+^T = C~^T P^-1 C~ (CovarianceTracker.covariance,
+ * tracking.py:88-119; identity of test_tracking.py:188-198): out [B][m][m]. */
+int rgb_covariance(const rgb_config *cfg, const rgb_state *state, void *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RGB_H_ */

@@ -1,0 +1,103 @@
+"""ctypes binding of librgb.so (include/rgb.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` /
+``python -m paper_2106_11594_b200._build``.  There is no CPU fallback: when the
+library or a CUDA device is missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librgb.so")
+
+RGB_ABI_VERSION = 1
+F64, F32 = 0, 1
+GENERAL, ORTHOGONAL, ORTHONORMAL = 0, 1, 2
+EPS_AUTO, EPS_FIXED = 0, 1
+OK, E_INVALID, E_UNSUPPORTED, E_CUDA = 0, -1, -2, -3
+ST_RANK_CAP, ST_NONFINITE, ST_BAD_ALPHA = 1, 2, 4
+
+EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest",
+           "rgb_project", "rgb_pinv", "rgb_covariance")
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("num_streams", ctypes.c_int64),
+        ("m", ctypes.c_int32),
+        ("k", ctypes.c_int32),
+        ("r_cap", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("variant", ctypes.c_int32),
+        ("eps_mode", ctypes.c_int32),
+        ("eps_value", ctypes.c_double),
+        ("alpha", ctypes.c_double),
+    ]
+
+
+class State(ctypes.Structure):
+    _fields_ = [
+        ("basis", ctypes.c_void_p),
+        ("dual", ctypes.c_void_p),
+        ("gram_inv", ctypes.c_void_p),
+        ("x", ctypes.c_void_p),
+        ("rank", ctypes.c_void_p),
+        ("nobs", ctypes.c_void_p),
+        ("status", ctypes.c_void_p),
+    ]
+
+
+class Logs(ctypes.Structure):
+    _fields_ = [
+        ("branch", ctypes.c_void_p),
+        ("coords", ctypes.c_void_p),
+        ("resid", ctypes.c_void_p),
+        ("gain", ctypes.c_void_p),
+    ]
+
+
+class RgbError(RuntimeError):
+    """A librgb.so call failed (RGB_E_UNSUPPORTED / RGB_E_CUDA)."""
+
+
+_LIB = None
+
+
+def load():
+    """Load librgb.so (raises if it was not built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RgbError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2106_11594_b200._build` "
+            "(there is no CPU fallback for the rank-Greville path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i64 = ctypes.c_void_p, ctypes.c_int64
+    cfgp, stp, lgp = ctypes.POINTER(Config), ctypes.POINTER(State), ctypes.POINTER(Logs)
+    lib.rgb_abi_version.restype = ctypes.c_int
+    lib.rgb_last_error.restype = ctypes.c_char_p
+    lib.rgb_state_reset.argtypes = [cfgp, stp, vp]
+    lib.rgb_ingest.argtypes = [cfgp, stp, vp, i64, vp, i64, i64, lgp, vp]
+    lib.rgb_project.argtypes = [cfgp, stp, vp, vp, vp, vp, vp, vp]
+    lib.rgb_pinv.argtypes = [cfgp, stp, vp, i64, vp, vp]
+    lib.rgb_covariance.argtypes = [cfgp, stp, vp, vp]
+    for name in EXPORTS[2:]:
+        getattr(lib, name).restype = ctypes.c_int
+    if lib.rgb_abi_version() != RGB_ABI_VERSION:
+        raise RgbError(f"librgb.so ABI {lib.rgb_abi_version()} != {RGB_ABI_VERSION}")
+    _LIB = lib
+    return lib
+
+
+def check(rc, what):
+    """Map a return code to the reference's exception types (solver.py:142-158)."""
+    if rc == OK:
+        return
+    msg = load().rgb_last_error().decode(errors="replace")
+    if rc == E_INVALID:
+        raise ValueError(f"{what}: {msg}")
+    raise RgbError(f"{what} failed ({rc}): {msg}")

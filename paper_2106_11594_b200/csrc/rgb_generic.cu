@@ -1,0 +1,245 @@
+// rgb_generic.cu -- shape-generic rank-Greville update kernel.
+//
+// One CTA per stream (grid-stride over streams), NT threads.  The factors
+// live in the caller's global buffers (L2 resident for the single-stream
+// configs), threads own strided columns j of C, C~, x; warps own rows i of
+// C~ and P^-1 for the reductions over m and r.  This kernel covers every
+// (m, r_cap, k, variant, dtype) the ABI accepts; the batched configurations
+// run on the specialised tensor-core kernel in rgb_blocked.cu.
+//
+// Per row it restates RecursiveSolver.ingest (solver.py:276-319):
+//   coords  = C~ a                       solver.py:286
+//   rej     = a - C^T coords, |rej|^2    solver.py:287-291
+//   test    rej^2 < eps^2 (1 + |a|^2)    solver.py:292-296
+//   dependent:   z = P coords, zs = z/(1+coords.z), P -= z zs^T,
+//                K = zs^T C~             solver.py:297-304
+//   independent: K = rej/|rej|^2 and _grow (solver.py:368-397)
+//   x += K (y - a.x)                     solver.py:303-304, 316-318
+#include "rgb_common.cuh"
+
+namespace rgb {
+
+constexpr int GEN_NT = 256;
+constexpr int GEN_NW = GEN_NT / 32;
+constexpr int GEN_MAX_K = 64;
+
+// Reduce `nv` per-thread partial sums held in smem-free fashion: each warp
+// reduces its lanes, lane 0 parks the result, then threads v < nv add the
+// per-warp partials.  `part(v)` returns this thread's partial for value v.
+template <typename REAL, typename F>
+__device__ __forceinline__ void block_reduce(int nv, REAL* red, REAL* out, F part) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int v = 0; v < nv; ++v) {
+    REAL s = warp_sum(part(v));
+    if (lane == 0) red[w * (GEN_MAX_K + 2) + v] = s;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < nv; v += GEN_NT) {
+    REAL s = 0;
+    for (int q = 0; q < GEN_NW; ++q) s += red[q * (GEN_MAX_K + 2) + v];
+    out[v] = s;
+  }
+  __syncthreads();
+}
+
+template <typename REAL>
+__global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
+    rgb_config cfg, rgb_state st, const REAL* __restrict__ rows, int64_t rows_stride,
+    const REAL* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
+  REAL* a_s = reinterpret_cast<REAL*>(smem_raw);        // m
+  REAL* rej_s = a_s + m;                                 // m
+  REAL* gam = rej_s + m;                                 // rc
+  REAL* z_s = gam + rc;                                  // rc
+  REAL* zs_s = z_s + rc;                                 // rc
+  REAL* y_s = zs_s + rc;                                 // k
+  REAL* sums = y_s + GEN_MAX_K;                          // k + 2: rej_sq, row_sq, a.x_c
+  REAL* red = sums + GEN_MAX_K + 2;                      // GEN_NW x (GEN_MAX_K + 2)
+  REAL* scal = red + GEN_NW * (GEN_MAX_K + 2);           // denom etc.
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+  for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
+    REAL* C = reinterpret_cast<REAL*>(st.basis) + b * (int64_t)rc * m;
+    REAL* D = (var == RGB_ORTHONORMAL) ? C : reinterpret_cast<REAL*>(st.dual) + b * (int64_t)rc * m;
+    REAL* P = reinterpret_cast<REAL*>(st.gram_inv) + b * (int64_t)rc * rc;
+    REAL* X = reinterpret_cast<REAL*>(st.x) + b * (int64_t)k * m;
+    const REAL* R = rows + b * rows_stride;
+    const REAL* Y = targets + b * tg_stride;
+    int r = st.rank[b];
+    int status = st.status[b];
+    int64_t nobs = st.nobs[b];
+    if (status) continue;
+    for (int64_t t = 0; t < T; ++t) {
+      const REAL* a = R + t * m;
+      for (int j = tid; j < m; j += GEN_NT) a_s[j] = a[j];
+      for (int c = tid; c < k; c += GEN_NT) y_s[c] = Y[t * k + c];
+      __syncthreads();
+      // coords = C~ a (solver.py:286): warp per dual row, lanes over columns
+      for (int i = w; i < r; i += GEN_NW) {
+        const REAL* d = D + (int64_t)i * m;
+        REAL s = 0;
+        for (int j = lane; j < m; j += 32) s = fma(d[j], a_s[j], s);
+        s = warp_sum(s);
+        if (lane == 0) gam[i] = s;
+      }
+      __syncthreads();
+      // rej = a - C^T coords (solver.py:287-288), kept for the independent branch
+      for (int j = tid; j < m; j += GEN_NT) {
+        REAL s = 0;
+        for (int i = 0; i < r; ++i) s = fma(gam[i], C[(int64_t)i * m + j], s);
+        rej_s[j] = a_s[j] - s;
+      }
+      __syncthreads();
+      // |rej|^2, |a|^2 and the k a-priori dot products a.x_c in one reduction
+      block_reduce<REAL>(2 + k, red, sums, [&](int v) {
+        REAL s = 0;
+        if (v == 0) {
+          for (int j = tid; j < m; j += GEN_NT) s = fma(rej_s[j], rej_s[j], s);
+        } else if (v == 1) {
+          for (int j = tid; j < m; j += GEN_NT) s = fma(a_s[j], a_s[j], s);
+        } else {
+          const REAL* xc = X + (int64_t)(v - 2) * m;
+          for (int j = tid; j < m; j += GEN_NT) s = fma(a_s[j], xc[j], s);
+        }
+        return s;
+      });
+      const REAL rej_sq = sums[0], row_sq = sums[1];
+      bool bad = !isfinite(row_sq);
+      for (int c = 0; c < k; ++c) bad |= !isfinite(y_s[c]);
+      if (bad) { status |= RGB_ST_NONFINITE; break; }
+      const bool dep = is_dependent<REAL>(rej_sq, row_sq, eps_sq<REAL>(cfg, r));
+      if (!dep && r >= rc) { status |= RGB_ST_RANK_CAP; break; }
+      if (logs.branch && tid == 0) logs.branch[b * T + t] = dep ? 0 : 1;
+      if (logs.resid)
+        for (int c = tid; c < k; c += GEN_NT)
+          reinterpret_cast<REAL*>(logs.resid)[(b * T + t) * k + c] = y_s[c] - sums[2 + c];
+      // z = P coords and denom = 1 + coords.z: dependent rows, and independent
+      // rows of the orthogonal/orthonormal variants (solver.py:298-299, 307-310)
+      const bool need_z = r > 0 && (dep || var != RGB_GENERAL);
+      if (need_z) {
+        for (int i = w; i < r; i += GEN_NW) {
+          const REAL* p = P + (int64_t)i * rc;
+          REAL s = 0;
+          for (int l = lane; l < r; l += 32) s = fma(p[l], gam[l], s);
+          s = warp_sum(s);
+          if (lane == 0) z_s[i] = s;
+        }
+        __syncthreads();
+        if (w == 0) {
+          REAL s = 0;
+          for (int i = lane; i < r; i += 32) s = fma(gam[i], z_s[i], s);
+          s = warp_sum(s);
+          if (lane == 0) scal[0] = (REAL)1 + s;
+        }
+        __syncthreads();
+      }
+      // rescaling of the stored rejection (orthogonal / orthonormal, solver.py:354-366, 383)
+      REAL alpha = 1, last = 1;
+      if (!dep && var != RGB_GENERAL) {
+        REAL resc;
+        if (var == RGB_ORTHONORMAL) resc = (REAL)1 / sqrt(rej_sq);          // solver.py:359-361
+        else resc = (REAL)cfg.alpha;                                          // solver.py:362-366
+        if (resc == (REAL)0) { status |= RGB_ST_BAD_ALPHA; break; }
+        last = (REAL)1 / resc;    // coords_row[r], solver.py:354
+        alpha = (REAL)1 / last;   // solver.py:383
+      }
+      if (logs.coords) {  // coords_row of _UpdateStep (solver.py:331, 344-355)
+        REAL* cl = reinterpret_cast<REAL*>(logs.coords) + (b * T + t) * rc;
+        for (int i = tid; i < rc; i += GEN_NT) {
+          REAL v = i < r ? gam[i] : (REAL)0;
+          if (!dep && var == RGB_GENERAL) v = (i == r) ? (REAL)1 : (REAL)0;
+          if (!dep && var != RGB_GENERAL && i == r) v = last;
+          cl[i] = v;
+        }
+      }
+      if (dep) {
+        if (r > 0) {
+          const REAL denom = scal[0];
+          for (int i = tid; i < r; i += GEN_NT) zs_s[i] = z_s[i] / denom;
+          __syncthreads();
+          for (int idx = tid; idx < r * r; idx += GEN_NT) {
+            int i = idx / r, l = idx - i * r;
+            P[(int64_t)i * rc + l] -= z_s[i] * zs_s[l];
+          }
+          for (int j = tid; j < m; j += GEN_NT) {
+            REAL g = 0;
+            for (int i = 0; i < r; ++i) g = fma(zs_s[i], D[(int64_t)i * m + j], g);
+            for (int c = 0; c < k; ++c) X[(int64_t)c * m + j] += g * (y_s[c] - sums[2 + c]);
+            if (logs.gain && t == T - 1) reinterpret_cast<REAL*>(logs.gain)[b * m + j] = g;
+          }
+        } else if (logs.gain && t == T - 1) {
+          for (int j = tid; j < m; j += GEN_NT) reinterpret_cast<REAL*>(logs.gain)[b * m + j] = 0;
+        }
+      } else {
+        // independent branch: gain = rej / |rej|^2 (solver.py:336) and _grow
+        for (int j = tid; j < m; j += GEN_NT) {
+          const REAL g = rej_s[j] / rej_sq;
+          if (var == RGB_GENERAL) {
+            for (int i = 0; i < r; ++i) D[(int64_t)i * m + j] -= gam[i] * g;   // solver.py:378
+            D[(int64_t)r * m + j] = g;                                          // solver.py:379
+            C[(int64_t)r * m + j] = a_s[j];                                     // solver.py:376
+          } else {
+            C[(int64_t)r * m + j] = alpha * rej_s[j];                           // solver.py:384
+            if (var == RGB_ORTHOGONAL) D[(int64_t)r * m + j] = rej_s[j] / (alpha * rej_sq);
+          }
+          for (int c = 0; c < k; ++c) X[(int64_t)c * m + j] += g * (y_s[c] - sums[2 + c]);
+          if (logs.gain && t == T - 1) reinterpret_cast<REAL*>(logs.gain)[b * m + j] = g;
+        }
+        for (int i = tid; i <= r; i += GEN_NT) {
+          REAL edge = 0, corner = 1;
+          if (var != RGB_GENERAL) {
+            if (i < r) edge = -(alpha * z_s[i]);
+            corner = alpha * alpha * (r > 0 ? scal[0] : (REAL)1);
+          }
+          if (i < r) {
+            P[(int64_t)i * rc + r] = edge;
+            P[(int64_t)r * rc + i] = edge;
+          } else {
+            P[(int64_t)r * rc + r] = corner;
+          }
+        }
+        r += 1;
+      }
+      nobs += 1;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      st.rank[b] = r;
+      st.nobs[b] = nobs;
+      st.status[b] = status;
+    }
+  }
+}
+
+size_t generic_smem_bytes(const rgb_config& cfg) {
+  size_t s = cfg.dtype == RGB_F32 ? 4 : 8;
+  size_t n = 2 * (size_t)cfg.m + 3 * (size_t)cfg.r_cap + GEN_MAX_K + (GEN_MAX_K + 2) +
+             GEN_NW * (GEN_MAX_K + 2) + 8;
+  return n * s;
+}
+
+int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                   const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                   cudaStream_t stream, int num_sms) {
+  if (cfg.k > GEN_MAX_K) return RGB_E_UNSUPPORTED;
+  size_t smem = generic_smem_bytes(cfg);
+  if (smem > 200 * 1024) return RGB_E_UNSUPPORTED;
+  int64_t grid = cfg.num_streams < (int64_t)num_sms * 8 ? cfg.num_streams : (int64_t)num_sms * 8;
+  if (grid < 1) return RGB_OK;
+  if (cfg.dtype == RGB_F64) {
+    auto kern = generic_ingest_kernel<double>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
+                                                   (const double*)targets, tg_stride, T, logs);
+  } else {
+    auto kern = generic_ingest_kernel<float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
+                                                  (const float*)targets, tg_stride, T, logs);
+  }
+  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+}  // namespace rgb

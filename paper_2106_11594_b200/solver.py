@@ -1,0 +1,257 @@
+"""Drop-in ``RecursiveSolver`` / ``solve_batch`` over the CUDA library.
+
+Same names, arguments, return types and exceptions as rankrls.solver
+(/root/reference/pkg/src/rankrls/solver.py), with the factors resident on the
+GPU and every update running in librgb.so (a one-stream ``BatchedSolver``):
+
+  RecursiveSolver(num_regressors, *, variant, eps, scalar, alpha)  solver.py:140-171
+  .update(row, target) -> UpdateReport                             solver.py:231-250
+  .ingest(rows, targets)                                           solver.py:252-319
+  .project(row) -> ProjectionResult / .is_dependent(proj, row)     solver.py:210-229
+  .solution .rank .num_observations .variant .scalar .eps_policy .basis()
+  solve_batch(matrix, targets, ...) -> (x, rank)                   solver.py:406-422
+
+Differences, all deliberate and documented in DESIGN.md:
+  * ``solution`` and ``basis()`` return read-only host copies, not live views;
+  * RATIONAL (exact mode) and callable ``alpha`` are CPU-only features of the
+    reference and raise CapabilityError here;
+  * the stored rank has a device capacity that doubles on demand, so streams
+    behave as if unbounded (the reference reallocates per row, solver.py:112-117).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .scalars import FLOAT32, FLOAT64, CapabilityError, ScalarKind
+
+VARIANTS = ("general", "orthogonal", "orthonormal")
+
+
+@dataclass(frozen=True)
+class EpsPolicy:
+    """Threshold policy (solver.py:32-72): auto / fixed / exact."""
+
+    mode: str
+    value: float | None = None
+
+    def __post_init__(self):
+        if self.mode not in ("auto", "fixed", "exact"):
+            raise ValueError(f"unknown eps mode {self.mode!r}")
+        if self.mode == "fixed":
+            if self.value is None or self.value < 0:
+                raise ValueError("fixed eps requires a nonnegative value")
+        elif self.value is not None:
+            raise ValueError(f"eps mode {self.mode!r} takes no value")
+
+    @classmethod
+    def auto(cls):
+        return cls("auto")
+
+    @classmethod
+    def fixed(cls, value):
+        return cls("fixed", float(value))
+
+    @classmethod
+    def exact_zero(cls):
+        return cls("exact")
+
+    def threshold(self, num_regressors, rank, machine_epsilon):
+        if self.mode == "fixed":
+            return self.value
+        if self.mode == "exact":
+            return 0.0
+        m, r = num_regressors, rank
+        return (m * m * r + m * r + m) * machine_epsilon
+
+
+@dataclass(frozen=True)
+class ProjectionResult:
+    coords: np.ndarray
+    rejection: np.ndarray
+    rejection_sq_norm: object
+
+
+@dataclass(frozen=True)
+class UpdateReport:
+    branch: str
+    gain: np.ndarray
+    predicted_residual: object
+    new_rank: int
+
+
+def _readonly(a):
+    a = np.array(a, copy=True)
+    a.flags.writeable = False
+    return a
+
+
+class RecursiveSolver:
+    """Online minimum-norm least squares on the GPU (drop-in for rankrls)."""
+
+    def __init__(self, num_regressors, *, variant="general", eps=None, scalar=FLOAT64, alpha=1,
+                 device=None, r_cap=None):
+        if not isinstance(num_regressors, (int, np.integer)) or num_regressors < 1:
+            raise ValueError(f"num_regressors must be a positive integer, got {num_regressors!r}")
+        if variant not in VARIANTS:
+            raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+        if not isinstance(scalar, ScalarKind):
+            raise TypeError(f"scalar must be a ScalarKind, got {scalar!r}")
+        if variant == "orthonormal" and not scalar.has_sqrt:
+            raise CapabilityError(
+                "the orthonormal variant needs square roots, which the "
+                f"{scalar.name!r} scalar kind does not provide")
+        if eps is None:
+            eps = EpsPolicy.exact_zero() if scalar.exact else EpsPolicy.auto()
+        if scalar.exact and eps.mode != "exact":
+            raise ValueError("exact rational scalars require the exact-zero eps policy")
+        if not scalar.exact and eps.mode == "exact":
+            raise ValueError("the exact-zero eps policy requires rational scalars")
+        if scalar.exact:
+            raise CapabilityError("exact rational arithmetic is CPU-only (use the reference rankrls)")
+        if callable(alpha):
+            raise CapabilityError("a callable orthogonal rescaling factor is not supported on the GPU")
+        import torch
+
+        from .batched import BatchedSolver
+
+        self._kind = scalar
+        self._variant = variant
+        self._eps = eps
+        self._alpha = alpha
+        self._m = int(num_regressors)
+        self._trackers = []
+        self._coords_chunks = []
+        tdtype = torch.float32 if scalar is FLOAT32 else torch.float64
+        cap = int(r_cap) if r_cap is not None else min(self._m, 32)
+        self._bs = BatchedSolver(1, self._m, k=1, r_cap=cap, variant=variant,
+                                 eps=None if eps.mode == "auto" else eps.value,
+                                 alpha=float(alpha), dtype=tdtype, device=device)
+        self._torch = torch
+        self._host = {"rank": 0, "nobs": 0}
+
+    # -- read-only access ---------------------------------------------------
+    @property
+    def num_regressors(self):
+        return self._m
+
+    @property
+    def rank(self):
+        return self._host["rank"]
+
+    @property
+    def num_observations(self):
+        return self._host["nobs"]
+
+    @property
+    def variant(self):
+        return self._variant
+
+    @property
+    def scalar(self):
+        return self._kind
+
+    @property
+    def eps_policy(self):
+        return self._eps
+
+    @property
+    def solution(self):
+        """Read-only host copy of the current minimum-norm solution."""
+        return _readonly(self._bs.x_t[0, 0].cpu().numpy())
+
+    def basis(self):
+        """Read-only host copies of (C, C_tilde, P_inv)."""
+        r = self.rank
+        C = self._bs.basis_t[0, :r].cpu().numpy()
+        D = C if self._variant == "orthonormal" else self._bs.dual_t[0, :r].cpu().numpy()
+        P = self._bs.gram_t[0, :r, :r].cpu().numpy()
+        return _readonly(C), _readonly(D), _readonly(P)
+
+    # -- core operations ------------------------------------------------------
+    def project(self, row):
+        """Coordinates of ``row`` in the stored basis plus its rejection."""
+        row = self._kind.vector(row, self._m)
+        t = self._torch.as_tensor(row, device=self._bs.device).view(1, self._m)
+        coords, rej, rsq, _ = self._bs.project(t)
+        r = self.rank
+        return ProjectionResult(coords[0, :r].cpu().numpy(), rej[0].cpu().numpy(),
+                                float(rsq[0].item()))
+
+    def is_dependent(self, proj, row):
+        """Rank test of solver.py:221-229 (a scalar decision, done on the host)."""
+        eps = self._eps.threshold(self._m, self.rank, self._kind.machine_epsilon)
+        eps_sq = eps * eps
+        rej_sq = float(proj.rejection_sq_norm)
+        row = np.asarray(row, dtype=np.float64)
+        row_sq = float(np.dot(row, row))
+        return rej_sq < eps_sq or rej_sq < eps_sq * row_sq
+
+    def update(self, row, target):
+        """Ingest one observation; returns an UpdateReport (solver.py:231-250)."""
+        row = self._kind.vector(row, self._m)
+        target = self._kind.coerce(target)
+        out = self._run(row[None, :], np.array([target], dtype=self._kind.dtype), want_report=True)
+        branch = "independent" if out["branch"][0] else "dependent"
+        return UpdateReport(branch, out["gain"], float(out["resid"][0]), self.rank)
+
+    def ingest(self, rows, targets):
+        """Fold a block of observations (solver.py:252-319); validated up front."""
+        A = self._kind.matrix(rows)
+        if A.shape[1] != self._m:
+            raise ValueError(f"rows have {A.shape[1]} columns, expected {self._m}")
+        y = self._kind.vector(targets, A.shape[0])
+        if A.shape[0]:
+            self._run(A, y, want_report=False)
+
+    # -- device plumbing --------------------------------------------------------
+    def _run(self, A, y, want_report):
+        torch = self._torch
+        bs = self._bs
+        dev = bs.device
+        n = A.shape[0]
+        rows = torch.as_tensor(np.ascontiguousarray(A, dtype=self._kind.dtype), device=dev)
+        tg = torch.as_tensor(np.ascontiguousarray(y, dtype=self._kind.dtype), device=dev)
+        done = 0
+        res = {}
+        while done < n:
+            T = n - done
+            log_coords = bool(self._trackers)
+            branch = torch.zeros((1, T), dtype=torch.uint8, device=dev)
+            resid = torch.zeros((1, T, 1), dtype=bs.dtype, device=dev)
+            coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=dev) if log_coords else None
+            gain = torch.zeros((1, self._m), dtype=bs.dtype, device=dev) if want_report else None
+            bs.ingest(rows[done:].view(1, T, self._m), tg[done:].view(1, T, 1), branch_log=branch,
+                      coords_log=coords, resid_log=resid, gain_out=gain)
+            nobs = int(bs.nobs_t[0].item())
+            consumed = nobs - self._host["nobs"]
+            self._host["nobs"] = nobs
+            self._host["rank"] = int(bs.rank_t[0].item())
+            if log_coords and consumed:
+                self._coords_chunks.append(coords[0, :consumed].cpu().numpy())
+            if want_report:
+                res = {"branch": branch[0, :consumed].cpu().numpy(), "resid": resid[0, :consumed, 0].cpu().numpy(),
+                       "gain": gain[0].cpu().numpy()}
+            done += consumed
+            status = int(bs.status_t[0].item())
+            if status & _lib.ST_RANK_CAP:
+                bs.grow(2 * bs.r_cap)
+                bs.status_t.zero_()
+            elif status:
+                bs.status_t.zero_()
+                raise ValueError(f"device status {status}: non-finite input or invalid rescaling factor")
+        return res
+
+
+def solve_batch(matrix, targets, *, variant="general", eps=None, scalar=FLOAT64, alpha=1):
+    """Fold all rows of a system through the solver; returns (x, rank) (solver.py:406-422)."""
+    A = scalar.matrix(matrix)
+    y = scalar.vector(targets)
+    if A.shape[0] != y.shape[0]:
+        raise ValueError(f"row count mismatch: matrix has {A.shape[0]} rows, targets {y.shape[0]}")
+    solver = RecursiveSolver(A.shape[1], variant=variant, eps=eps, scalar=scalar, alpha=alpha)
+    solver.ingest(A, y)
+    return np.array(solver.solution, copy=True), solver.rank

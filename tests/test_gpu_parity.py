@@ -1,0 +1,290 @@
+"""GPU parity: librgb.so against the reference's golden vectors and the C oracle.
+
+Bar (BASELINE.json north star): identical detected ranks and branch
+sequences; x and A+ within 1e-9 relative (fp64), 1e-3 (fp32), with the error
+metric of test_acceptance.py:56-61.  Rows whose oracle rank-test margin
+rho = |rej| / (eps max(1, |a|)) lies in [1/4, 4] are "ambiguous": they are
+counted and reported, and strict branch equality is asserted on the others.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from rgb_testutil import relerr, residual_error
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-9
+TOL32 = 1e-3
+
+
+def dev(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+def run_batched(rows, targets, *, r_cap, variant="general", eps=None, dtype=torch.float64, logs=True):
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    rows = np.asarray(rows)
+    targets = np.asarray(targets)
+    if rows.ndim == 2:
+        rows, targets = rows[None], targets[None]
+    if targets.ndim == 2:
+        targets = targets[..., None]
+    B, T, m = rows.shape
+    k = targets.shape[-1]
+    bs = BatchedSolver(B, m, k=k, r_cap=r_cap, variant=variant, eps=eps, dtype=dtype)
+    out = {}
+    if logs:
+        out["branch"] = torch.zeros((B, T), dtype=torch.uint8, device="cuda")
+        out["coords"] = torch.zeros((B, T, r_cap), dtype=dtype, device="cuda")
+        out["resid"] = torch.zeros((B, T, k), dtype=dtype, device="cuda")
+    bs.ingest(dev(rows, dtype), dev(targets, dtype), branch_log=out.get("branch"),
+              coords_log=out.get("coords"), resid_log=out.get("resid"))
+    torch.cuda.synchronize()
+    res = {key: v.cpu().numpy() for key, v in out.items()}
+    res.update(x=bs.solution.cpu().numpy(), rank=bs.rank.cpu().numpy(), nobs=bs.nobs_t.cpu().numpy(),
+               status=bs.status.cpu().numpy(), solver=bs)
+    return res
+
+
+# -- golden vectors produced by the reference ------------------------------------
+
+def test_c1_golden_branches_rank_x_pinv(golden):
+    g = golden("c1.npz")
+    res = run_batched(g["A"], g["y"], r_cap=64)
+    assert int(res["rank"][0]) == int(g["rank"]) == 16
+    assert np.array_equal(res["branch"][0], g["branch"])
+    assert relerr(res["x"][0, :, 0], g["x"]) <= TOL64
+    pinv = res["solver"].pinv(dev(res["coords"])).cpu().numpy()[0]
+    assert relerr(pinv, g["pinv"]) <= TOL64
+
+
+@pytest.mark.parametrize("name,r_cap", [("c5_sample.npz", 16), ("c3_sample.npz", 32)])
+def test_batched_golden_samples(golden, name, r_cap):
+    g = golden(name)
+    res = run_batched(g["rows"], g["targets"], r_cap=r_cap)
+    assert np.array_equal(res["rank"], g["rank"])
+    assert np.array_equal(res["branch"], g["branch"])
+    assert (res["status"] == 0).all()
+    for b in range(res["x"].shape[0]):
+        assert relerr(res["x"][b], g["x"][b]) <= TOL64
+
+
+@pytest.mark.parametrize("variant", ["general", "orthogonal", "orthonormal"])
+def test_variants_golden_through_compat_api(golden, variant):
+    import paper_2106_11594_b200 as p
+
+    g = golden("variants.npz")
+    for case in range(12):
+        A, y = g[f"A{case}"], g[f"y{case}"]
+        x, rank = p.solve_batch(A, y, variant=variant)
+        assert rank == int(g[f"{variant}_rank{case}"])
+        assert relerr(x, g[f"{variant}_x{case}"]) <= TOL64
+        assert relerr(p.pinv_from_scratch(A, variant=variant), g[f"{variant}_pinv{case}"]) <= TOL64
+        s = p.RecursiveSolver(A.shape[1], variant=variant)
+        branches = [s.update(row, t).branch == "independent" for row, t in zip(A, y)]
+        assert np.array_equal(np.array(branches, np.uint8), g[f"{variant}_branch{case}"])
+
+
+def test_kahan_absolute_clause_and_stability(golden):
+    import paper_2106_11594_b200 as p
+
+    g = golden("kahan.npz")
+    K = g["K"]
+    s = p.RecursiveSolver(100, eps=p.EpsPolicy.fixed(1e-8))
+    s.ingest(K, np.zeros(100))
+    assert s.rank == int(g["rank_fixed"]) == 99
+    pinv = p.pinv_from_scratch(K)
+    assert residual_error(pinv, K) <= 1e-14
+    assert relerr(pinv, g["pinv_auto"]) <= 1e-6   # kappa_2(K) = 2.2e9
+
+
+# -- known answers (test_solver.py / test_tracking.py) ---------------------------
+
+def test_update_sequence_known_answers():
+    import paper_2106_11594_b200 as p
+
+    s = p.RecursiveSolver(2)
+    rep = s.update([1, 0], 2.0)
+    assert rep.branch == "independent" and rep.new_rank == 1
+    assert np.allclose(s.solution, [2, 0])
+    rep = s.update([1, 0], 4.0)
+    assert rep.branch == "dependent" and rep.new_rank == 1
+    assert np.allclose(rep.gain, [0.5, 0])
+    assert np.allclose(s.solution, [3, 0])
+    rep = s.update([1, 1], 5.0)
+    assert rep.branch == "independent" and rep.new_rank == 2
+    assert np.allclose(rep.gain, [0, 1])
+    assert np.allclose(s.solution, [3, 2])
+    assert s.num_observations == 3
+    before = s.solution.copy()
+    rep = s.update([2, 1], 1.0)
+    assert np.allclose(before + rep.gain * rep.predicted_residual, s.solution)
+
+
+def test_zero_rows_duplicates_and_errors():
+    import paper_2106_11594_b200 as p
+
+    s = p.RecursiveSolver(2)
+    rep = s.update([0, 0], 7.0)
+    assert rep.branch == "dependent" and s.rank == 0 and np.allclose(rep.gain, [0, 0])
+    s.update([1, 0], 2.0)
+    x = s.solution.copy()
+    assert s.update([0, 0], -3.0).branch == "dependent"
+    assert np.array_equal(s.solution, x)
+    x, rank = p.solve_batch([[1, 0], [1, 0]], [0, 2])
+    assert np.allclose(x, [1, 0]) and rank == 1
+    x, rank = p.solve_batch(np.eye(2), [3, 4])
+    assert np.allclose(x, [3, 4]) and rank == 2
+    with pytest.raises(ValueError):
+        p.solve_batch(np.eye(2), [1, 2, 3])
+    with pytest.raises(ValueError):
+        s.update([1, 2, 3], 0.0)
+    with pytest.raises(ValueError):
+        s.update([np.nan, 0], 0.0)
+    with pytest.raises(ValueError):
+        s.update([1, 0], np.inf)
+    with pytest.raises(ValueError):
+        s.solution[0] = 5.0
+
+
+def test_projection_and_trackers_known_answers():
+    import paper_2106_11594_b200 as p
+
+    s = p.RecursiveSolver(3)
+    s.update([1, 0, 0], 0.0)
+    proj = s.project([2, 3, 0])
+    assert np.allclose(proj.coords, [2]) and np.allclose(proj.rejection, [0, 3, 0])
+    assert proj.rejection_sq_norm == pytest.approx(9.0)
+    assert not s.is_dependent(proj, np.array([2.0, 3, 0]))
+    assert s.is_dependent(s.project([5, 0, 0]), np.array([5.0, 0, 0]))
+    s2 = p.RecursiveSolver(2)
+    tr = p.PseudoinverseTracker(s2)
+    s2.update([1, 1], 0.0)
+    assert np.allclose(tr.pinv, [[0.5], [0.5]])
+    s2.update([0, 0], 5.0)
+    assert tr.pinv.shape == (2, 2) and np.array_equal(tr.pinv[:, 1], [0, 0])
+    with pytest.raises(ValueError):
+        p.PseudoinverseTracker(s2)
+    assert np.array_equal(p.pinv_from_scratch(np.zeros((2, 3))), np.zeros((3, 2)))
+    assert np.allclose(p.pinv_from_scratch([[1.0, 1.0], [1.0, 1.0]]), 0.25 * np.ones((2, 2)))
+    s3 = p.RecursiveSolver(2)
+    cov = p.CovarianceTracker(s3)
+    s3.update([1, 1], 0.0)
+    assert np.allclose(cov.covariance, 0.25 * np.ones((2, 2)))
+
+
+def test_rank_capacity_grows_like_the_reference():
+    import paper_2106_11594_b200 as p
+
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((60, 50))
+    y = rng.standard_normal(60)
+    s = p.RecursiveSolver(50, r_cap=4)
+    s.ingest(A, y)
+    assert s.rank == 50 and s.num_observations == 60
+    o = oracle.ingest(A[None], y[None], r_cap=64)
+    assert relerr(s.solution, oracle.solution(o)[0, :, 0]) <= TOL64
+
+
+# -- full-size configurations against the C oracle --------------------------------
+
+def ambiguous_rows(rho):
+    return (rho >= 0.25) & (rho <= 4.0)
+
+
+def compare_to_oracle(rows, targets, res, r_cap, tol=TOL64, variant="general"):
+    o = oracle.ingest(rows, targets, r_cap=r_cap, variant=variant, nthreads=8)
+    amb_rows = ambiguous_rows(o["rho"])
+    amb = amb_rows.any(axis=1) | (o["status"] != 0) | (res["status"] != 0)
+    ok = ~amb
+    assert np.array_equal(res["rank"][ok], o["rank"][ok])
+    assert np.array_equal(res["branch"][ok], o["branch"][ok])
+    X = oracle.solution(o)
+    worst = max((relerr(res["x"][b], X[b]) for b in np.nonzero(ok)[0]), default=0.0)
+    assert worst <= tol, worst
+    return int(amb.sum()), worst
+
+
+def test_c5_full_length_streams_against_oracle():
+    from paper_2106_11594_b200 import workloads
+
+    streams = list(range(64))
+    rows, tg = workloads.host_batch("c5", streams)
+    res = run_batched(rows, tg, r_cap=16)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16)
+    assert amb <= 2
+    assert (res["rank"][res["status"] == 0] == 16).all()
+
+
+def test_c3_full_length_streams_against_oracle():
+    from paper_2106_11594_b200 import workloads
+
+    streams = list(range(32))
+    rows, tg = workloads.host_batch("c3", streams)
+    res = run_batched(rows, tg, r_cap=32)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=32)
+    assert amb <= 1
+
+
+def test_device_generated_c5_sample_against_oracle():
+    """Streams generated on the GPU exactly as bench.py does; the oracle reads
+    the same bytes back."""
+    from paper_2106_11594_b200 import workloads
+
+    rows_d, tg_d = workloads.device_batch("c5", 4096, 4096 + 48, "cuda")
+    rows, tg = rows_d.cpu().numpy(), tg_d.cpu().numpy()
+    res = run_batched(rows, tg, r_cap=16)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16)
+    assert amb <= 2
+
+
+def test_multi_rhs_equals_single_rhs_runs(golden):
+    g = golden("c5_sample.npz")
+    full = run_batched(g["rows"], g["targets"], r_cap=16, logs=False)
+    for c in (0, 5):
+        one = run_batched(g["rows"], g["targets"][:, :, c], r_cap=16, logs=False)
+        assert relerr(one["x"][:, :, 0], full["x"][:, :, c]) <= 1e-13
+
+
+def test_fp32_integer_streams_track_fp64(golden):
+    g = golden("c5_sample.npz")
+    odd = [1, 3, 5]
+    rows, tg = g["rows"][odd], g["targets"][odd]
+    res = run_batched(rows, tg, r_cap=16, dtype=torch.float32)
+    assert (res["rank"] == 16).all()
+    assert np.array_equal(res["branch"], g["branch"][odd])
+    for i in range(len(odd)):
+        assert relerr(res["x"][i], g["x"][odd[i]]) <= TOL32
+
+
+def test_status_bits_rank_cap_and_nonfinite():
+    rows = np.eye(4)[None].repeat(2, axis=0)
+    tg = np.ones((2, 4, 1))
+    tg[1, 1, 0] = np.nan
+    res = run_batched(rows, tg, r_cap=2)
+    assert res["status"][0] == 1 and res["rank"][0] == 2 and res["nobs"][0] == 2
+    assert res["status"][1] == 2 and res["rank"][1] == 1 and res["nobs"][1] == 1
+
+
+def test_invariants_after_full_c5_ingest():
+    """Size-independent properties at full stream length: C~ C^T = I,
+    P symmetric, x in the row space, re-ingesting rows is all dependent."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch("c5", [6, 7])
+    res = run_batched(rows, tg, r_cap=16)
+    bs = res["solver"]
+    C = bs.basis_t.cpu().numpy(); D = bs.dual_t.cpu().numpy(); P = bs.gram_t.cpu().numpy()
+    for b in range(2):
+        assert np.abs(D[b] @ C[b].T - np.eye(16)).max() <= 1e-9
+        assert np.abs(P[b] - P[b].T).max() <= 1e-12 * max(1.0, np.abs(P[b]).max())
+    X = res["x"]
+    bs.ingest(dev(rows[:, :64]), dev(tg[:, :64]))
+    br = torch.zeros((2, 64), dtype=torch.uint8, device="cuda")
+    bs.ingest(dev(rows[:, 64:128]), dev(tg[:, 64:128]), branch_log=br)
+    assert int(br.sum()) == 0 and (bs.rank.cpu().numpy() == 16).all()
+    assert np.isfinite(X).all()
