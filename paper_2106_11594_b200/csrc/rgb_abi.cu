@@ -118,9 +118,10 @@ int rgb_ingest(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t r
   rgb_state s2 = *st;
   if (cfg->variant == RGB_ORTHONORMAL) s2.dual = s2.basis;  // C~ is C (solver.py:168, 386)
   cudaStream_t s = (cudaStream_t)stream;
-  if (rgb::blocked_supports(*cfg))
+  rc = RGB_E_UNSUPPORTED;
+  if (rgb::blocked_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
-  else
+  if (rc == RGB_E_UNSUPPORTED)
     rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
   if (rc == RGB_E_UNSUPPORTED) return fail(rc, "shape beyond kernel limits (k <= 64, smem)");
   if (rc == RGB_E_CUDA) return cuda_fail(cudaGetLastError(), "rgb_ingest launch");

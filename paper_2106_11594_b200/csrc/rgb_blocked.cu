@@ -1,10 +1,536 @@
-// rgb_blocked.cu -- placeholder until the tensor-core blocked kernel lands.
+// rgb_blocked.cu -- batched rank-Greville update on fp64 tensor cores (sm_100a).
+//
+// One warp owns one stream at a time (persistent grid, static round-robin over
+// streams) and consumes its rows in tiles of 8.  Inside a run of dependent
+// rows the basis C and dual C~ do not change (solver.py:297-304 touch only
+// P^-1 and x), so the per-row GEMVs of the reference become 8-row contractions
+// on DMMA.8x8x4 (mma.sync m8n8k4 f64), with every reduction inside the tensor
+// core instead of in warp shuffles:
+//
+//   G   = A C~^T                 coords of the 8 rows      (solver.py:286)
+//   R   = A - G C, |R_t|^2       rejections and the test   (solver.py:287-296)
+//   U   = P G^T,  S = G P G^T    Sherman-Morrison inputs   (solver.py:298-299)
+//   M   = I + S = L diag(d) L^T  8x8 LDL^T by elimination in registers, E = L^-1
+//   Y^T = U E^T                  columns = the z_t of the 8 sequential steps
+//   P  -= Y^T D^-1 Y             = 8 sequential rank-1 updates of solver.py:300-301
+//   W  += Y^T D^-1 E dy0         the 8 solution updates of solver.py:302-304
+//
+// This is the reference's 8 sequential Sherman-Morrison steps in factored
+// (LDL^T) form -- identical algebra, the same accuracy as the
+// sequential recursion (an explicit M^-1 / Woodbury update is not; see
+// DESIGN.md), and every contraction on the tensor cores (the blocked variant
+// of SURVEY.md section 7, hard part 5).  The solution is carried as
+// x = x0 + C~^T W (W is r x k): a dependent row changes only W, an independent
+// row appends W's row r = y - a.x0 (exact algebra for x' = x + K dy with
+// C~' = [C~ - gamma K^T; K^T]), and x is materialised once at the end of the
+// call.  dy0 = y - a.x0 - gamma^T W is the reference's a-priori residual.
+//
+// Independent rows (solver.py:305-318, _grow solver.py:368-397) split the tile:
+// the dependent prefix is folded, the row grows the basis (K = rej/|rej|^2,
+// C~[:r] -= gamma K^T, C~[r] = K, C[r] = a, P = diag(P, 1)), and the rest of
+// the tile is re-projected on the new basis.  Rank tests use the reference's
+// threshold with the CURRENT rank for every row (solver.py:292-296).
+//
+// Fragment layouts (m8n8k4 f64; lane = 4p + q): A[m=p][k=q], B[k=q][n=p],
+// C/D[m=p][n=2q+e].  K slots are permuted, sigma(kt,q) = 8(kt>>1)+2q+(kt&1),
+// so that every accumulator is directly the next MMA's operand:
+//   tile   a[nt][e]      = A[t=p][8nt+2q+e]            (A- and B-operand, K=sigma)
+//   C~^T   Dt[nt][kt]    = C~[8nt+p][sigma(kt,q)]       registers
+//   C      Cs[kt][jt][l] = C[sigma(kt,q)][8jt+p]        shared memory
+//   P^-1   Pr[mt][nt][e] = P[8mt+p][8nt+2q+e]           registers (symmetric)
+//   W^T    Wt[nt][e]     = W[8nt+2q+e][c=p]             registers
+//
+// Specialised for the batched configuration m = 64, r_cap = 16, k = 8 (fp64,
+// general variant); every other shape runs on rgb_generic.cu.
 #include "rgb_common.cuh"
 
 namespace rgb {
-bool blocked_supports(const rgb_config&) { return false; }
-int launch_blocked(const rgb_config&, rgb_state&, const void*, int64_t, const void*, int64_t, int64_t,
-                   const rgb_logs&, cudaStream_t, int) {
-  return RGB_E_UNSUPPORTED;
+namespace blk {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TT = 8;  // rows per tile
+
+__device__ __forceinline__ void mma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
 }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int sigma(int kt, int q) { return 8 * (kt >> 1) + 2 * q + (kt & 1); }
+
+template <int M, int R, int KC>
+struct WarpSmem {
+  double Cs[R / 4][M / 8][32];   // basis C as the B operand of R = A - G C
+  double At[2][M / 8][32][2];    // double-buffered row tile, lane-slot layout
+  double Yt[2][32][2];           // targets y[t=2q+e][c=p]
+  union {
+    struct {
+      double gam[R];             // coords of an independent row
+      double kv[M];              // its gain K = rej / |rej|^2
+      double av[M];              // the row itself
+    } ind;
+    double w[R][KC];             // W at the end of the call
+  } u;
+};
+
+template <int M, int R, int KC, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) blocked_kernel(
+    rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
+    const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
+    double* __restrict__ clog) {
+  static_assert(M % 8 == 0 && R % 8 == 0 && KC == 8, "shape");
+  constexpr int JT = M / 8, JK = M / 4, IT = R / 8, IK = R / 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = lane >> 2, q = lane & 3;
+  WarpSmem<M, R, KC>& S = reinterpret_cast<WarpSmem<M, R, KC>*>(smem_raw)[wid];
+  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+
+  for (int64_t b = (int64_t)blockIdx.x * WARPS + wid; b < cfg.num_streams; b += nwarps) {
+    int status = st.status[b];
+    if (status) continue;
+    int r = st.rank[b];
+    const int64_t nobs0 = st.nobs[b];
+    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
+    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
+    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
+    double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)KC * M;
+    const double* Rb = rows + b * rstride;
+    const double* Yb = tgts + b * tstride;
+
+    // ---- load the stream's state into fragment layouts -------------------------
+    double Dt[IT][JK];
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+      for (int J = 0; J < JK / 2; ++J) {
+        double2 v = *reinterpret_cast<const double2*>(Dg + (8 * nt + p) * M + 8 * J + 2 * q);
+        Dt[nt][2 * J] = v.x;
+        Dt[nt][2 * J + 1] = v.y;
+      }
+    double Pr[IT][IT][2];
+#pragma unroll
+    for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        double2 v = *reinterpret_cast<const double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q);
+        Pr[mt][nt][0] = v.x;
+        Pr[mt][nt][1] = v.y;
+      }
+#pragma unroll
+    for (int kt = 0; kt < IK; ++kt)
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) S.Cs[kt][jt][lane] = Cg[sigma(kt, q) * M + 8 * jt + p];
+    double Wt[IT][2];
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt) Wt[nt][0] = Wt[nt][1] = 0.0;
+    // x0 = the solution at call start; when it is exactly zero (a fresh
+    // stream) a.x0 = 0 and its contraction is skipped.
+    bool nz = false;
+#pragma unroll
+    for (int J = 0; J < JK / 2; ++J) {
+      double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q);
+      nz |= (v.x != 0.0) || (v.y != 0.0);
+    }
+    const bool has_x0 = __any_sync(FULL, nz);
+    __syncwarp();
+
+    // ---- tile loop ----------------------------------------------------------------
+    const int64_t ntiles = (T + TT - 1) / TT;
+    int64_t consumed = 0;
+    auto prefetch = [&](int64_t tile, int s) {
+      const int64_t t0 = tile * TT;
+      const int64_t t = t0 + p;
+      const bool ok = t < T;
+      const double* src = ok ? Rb + t * M : Rb;
+#pragma unroll
+      for (int nt = 0; nt < JT; ++nt) cp_async16(&S.At[s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t ty = t0 + 2 * q + e;
+        const bool oky = ty < T;
+        cp_async8(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky ? 8 : 0);
+      }
+      cp_commit();
+    };
+    if (ntiles > 0) prefetch(0, 0);
+    bool stopped = false;
+    for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
+      const int s = (int)(tile & 1);
+      if (tile + 1 < ntiles) {
+        prefetch(tile + 1, s ^ 1);
+        cp_wait<1>();
+      } else {
+        cp_wait<0>();
+      }
+      double a[JT][2];
+#pragma unroll
+      for (int nt = 0; nt < JT; ++nt) {
+        double2 v = *reinterpret_cast<const double2*>(&S.At[s][nt][lane][0]);
+        a[nt][0] = v.x;
+        a[nt][1] = v.y;
+      }
+      double yv[2];
+      {
+        double2 v = *reinterpret_cast<const double2*>(&S.Yt[s][lane][0]);
+        yv[0] = v.x;
+        yv[1] = v.y;
+      }
+      const int64_t t0 = tile * TT;
+      const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
+
+      // row norms |a_t|^2 (solver.py:267), quad-reduced: all 4 lanes of row p
+      double asq = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < JT; ++nt) asq = fma(a[nt][0], a[nt][0], fma(a[nt][1], a[nt][1], asq));
+      asq += __shfl_xor_sync(FULL, asq, 1);
+      asq += __shfl_xor_sync(FULL, asq, 2);
+      // non-finite targets, per row (scalars.py:122-123 rejects them)
+      const unsigned yb0 = __ballot_sync(FULL, !isfinite(yv[0]));
+      const unsigned yb1 = __ballot_sync(FULL, !isfinite(yv[1]));
+      const bool ybad = (((p & 1) ? yb1 : yb0) & (0x11111111u << (p >> 1))) != 0u;
+      // dyx = y - a.x0 for (c = p, t = 2q + e)
+      double dyx[2] = {yv[0], yv[1]};
+      if (has_x0) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int J = 0; J < JK / 2; ++J) {
+          double2 xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q));
+          mma(acc, xv.x, a[J][0]);
+          mma(acc, xv.y, a[J][1]);
+        }
+        dyx[0] -= acc[0];
+        dyx[1] -= acc[1];
+      }
+
+      int row_start = 0;
+      while (true) {
+        // G = A C~^T : M = t, N = i, K = j
+        double g[IT][2], g2[IT][2];
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = g2[nt][0] = g2[nt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < JK; kt += 2)
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            mma(g[nt], a[kt >> 1][0], Dt[nt][kt]);
+            mma(g2[nt], a[kt >> 1][1], Dt[nt][kt + 1]);
+          }
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          g[nt][0] += g2[nt][0];
+          g[nt][1] += g2[nt][1];
+        }
+        // R = A - G C and |R_t|^2 : M = t, N = j, K = i
+        double rsq = 0.0;
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+          double acc[2] = {0.0, 0.0};
+#pragma unroll
+          for (int kt = 0; kt < IK; ++kt) mma(acc, g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+          const double r0 = a[jt][0] - acc[0], r1 = a[jt][1] - acc[1];
+          rsq = fma(r0, r0, fma(r1, r1, rsq));
+        }
+        rsq += __shfl_xor_sync(FULL, rsq, 1);
+        rsq += __shfl_xor_sync(FULL, rsq, 2);
+        // rank test per row with the current rank
+        const double esq = eps_sq<double>(cfg, r);
+        const bool valid = p >= row_start && p < tv;
+        const bool dep = is_dependent<double>(rsq, asq, esq);
+        const bool bad = !isfinite(asq) || ybad;
+        const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
+        const unsigned badm = __ballot_sync(FULL, q == 0 && valid && bad);
+        const int tstar = stopm ? (__ffs(stopm) - 1) >> 2 : tv;
+
+        if (tstar > row_start) {
+          // ---- dependent rows [row_start, tstar): blocked Sherman-Morrison --------
+          const bool inb = p >= row_start && p < tstar;
+          double gm[IT][2];
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            gm[nt][0] = inb ? g[nt][0] : 0.0;
+            gm[nt][1] = inb ? g[nt][1] : 0.0;
+          }
+          // dy0^T = dyx - (G W)^T : M = c, N = t, K = i
+          double dy[2];
+          {
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kt = 0; kt < IK; ++kt) mma(acc, Wt[kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int t = 2 * q + e;
+              dy[e] = (t >= row_start && t < tstar) ? dyx[e] - acc[e] : 0.0;
+            }
+          }
+          // U = P G^T (M = i, N = t) and U^T = G P (M = t, N = i)
+          double u[IT][2], ut[IT][2];
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt) {
+            u[mt][0] = u[mt][1] = ut[mt][0] = ut[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < IK; ++kt) {
+              mma(u[mt], Pr[mt][kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
+              mma(ut[mt], gm[kt >> 1][kt & 1], Pr[mt][kt >> 1][kt & 1]);
+            }
+          }
+          // M = I + G P G^T  (8 x 8, M = t, N = t')
+          double mi[2] = {0.0, 0.0};
+#pragma unroll
+          for (int kt = 0; kt < IK; ++kt) mma(mi, ut[kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
+          if (p == 2 * q) mi[0] += 1.0;
+          if (p == 2 * q + 1) mi[1] += 1.0;
+          // M = L diag(d) L^T by forward elimination on [M | I]: E = L^-1
+          // (unit lower), d = pivots.  This is the 8-step Sherman-Morrison
+          // recursion in factored form: z_t = (U E^T)_t / d_t exactly as the
+          // sequential steps of solver.py:298-301 (an explicit M^-1 loses
+          // accuracy when M is ill-conditioned; the factored form does not).
+          double ev[2] = {p == 2 * q ? 1.0 : 0.0, p == 2 * q + 1 ? 1.0 : 0.0};
+#pragma unroll
+          for (int k = 0; k < TT - 1; ++k) {
+            const double v = (k & 1) ? mi[1] : mi[0];
+            const double piv = __shfl_sync(FULL, v, 4 * k + (k >> 1));
+            const double mps = __shfl_sync(FULL, v, 4 * p + (k >> 1));
+            const double m0 = __shfl_sync(FULL, mi[0], 4 * k + q);
+            const double m1 = __shfl_sync(FULL, mi[1], 4 * k + q);
+            const double e0 = __shfl_sync(FULL, ev[0], 4 * k + q);
+            const double e1 = __shfl_sync(FULL, ev[1], 4 * k + q);
+            if (p > k) {
+              const double f = mps / piv;
+              mi[0] = fma(-f, m0, mi[0]);
+              mi[1] = fma(-f, m1, mi[1]);
+              ev[0] = fma(-f, e0, ev[0]);
+              ev[1] = fma(-f, e1, ev[1]);
+            }
+          }
+          // 1/d_t for t = p (quad-shared) and for t = 2q, 2q + 1
+          const double dsel = (p & 1) ? mi[1] : mi[0];
+          const double rd = 1.0 / __shfl_sync(FULL, dsel, 4 * p + (p >> 1));
+          const double rd0 = __shfl_sync(FULL, rd, 8 * q);
+          const double rd1 = __shfl_sync(FULL, rd, 8 * q + 4);
+          // Y^T = U E^T (M = i, N = t, K = t'): column t is z_t of the sequential form
+          double yt[IT][2];
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt) {
+            yt[mt][0] = yt[mt][1] = 0.0;
+            mma(yt[mt], u[mt][0], ev[0]);
+            mma(yt[mt], u[mt][1], ev[1]);
+          }
+          // E dy0 (M = c, N = t, K = t'): the a-priori residuals of the 8 rows
+          double dh[2] = {0.0, 0.0};
+          mma(dh, dy[0], ev[0]);
+          mma(dh, dy[1], ev[1]);
+          dh[0] *= rd0;
+          dh[1] *= rd1;
+          // P -= Y^T D^-1 Y   and   W^T += (E dy0)^T D^-1 Y
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt) {
+            const double s0 = -yt[mt][0] * rd0, s1 = -yt[mt][1] * rd1;
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt) {
+              mma(Pr[mt][nt], s0, yt[nt][0]);
+              mma(Pr[mt][nt], s1, yt[nt][1]);
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            mma(Wt[nt], dh[0], yt[nt][0]);
+            mma(Wt[nt], dh[1], yt[nt][1]);
+          }
+          // logs: branch 0, coordinate row gamma_t (zero beyond the rank)
+          if (inb) {
+            const int64_t row = b * T + t0 + p;
+            if (blog && q == 0) blog[row] = 0;
+            if (clog) {
+#pragma unroll
+              for (int nt = 0; nt < IT; ++nt)
+                *reinterpret_cast<double2*>(clog + row * R + 8 * nt + 2 * q) = make_double2(g[nt][0], g[nt][1]);
+            }
+          }
+        }
+        if (tstar >= tv) break;
+
+        // ---- row tstar: non-finite input or rank growth ------------------------------
+        if ((badm >> (4 * tstar)) & 1u) {
+          status |= RGB_ST_NONFINITE;
+          consumed = t0 + tstar;
+          stopped = true;
+          break;
+        }
+        if (r >= R) {
+          status |= RGB_ST_RANK_CAP;
+          consumed = t0 + tstar;
+          stopped = true;
+          break;
+        }
+        {
+          // rejection of row tstar on the current basis (recomputed: rare path)
+          const double rs = __shfl_sync(FULL, rsq, 4 * tstar);
+          if (p == tstar) {
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt) {
+              S.u.ind.gam[8 * nt + 2 * q] = g[nt][0];
+              S.u.ind.gam[8 * nt + 2 * q + 1] = g[nt][1];
+            }
+          }
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kt = 0; kt < IK; ++kt) mma(acc, g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+            if (p == tstar) {
+              S.u.ind.kv[8 * jt + 2 * q] = (a[jt][0] - acc[0]) / rs;
+              S.u.ind.kv[8 * jt + 2 * q + 1] = (a[jt][1] - acc[1]) / rs;
+              S.u.ind.av[8 * jt + 2 * q] = a[jt][0];
+              S.u.ind.av[8 * jt + 2 * q + 1] = a[jt][1];
+            }
+          }
+          __syncwarp();
+          // W gains row r: y - a.x0 of row tstar (x = x0 + C~^T W stays exact)
+          const double dv = (tstar & 1) ? dyx[1] : dyx[0];
+          const double wnew = __shfl_sync(FULL, dv, 4 * p + (tstar >> 1));
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (8 * nt + 2 * q + e == r) Wt[nt][e] = wnew;
+          // C~[:r] -= gamma K^T, C~[r] = K   (solver.py:377-380)
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            const int i = 8 * nt + p;
+            const double gi = S.u.ind.gam[i];
+#pragma unroll
+            for (int J = 0; J < JK / 2; ++J) {
+              const double2 kv = *reinterpret_cast<const double2*>(&S.u.ind.kv[8 * J + 2 * q]);
+              Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
+              Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
+            }
+          }
+          // C[r] = a  (solver.py:376)
+          if (q == ((r & 7) >> 1)) {
+            const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+            for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = S.u.ind.av[8 * jt + p];
+          }
+          // P = diag(P, 1)  (solver.py:372-373, 381)
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
+                if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
+              }
+          const int64_t row = b * T + t0 + tstar;
+          if (blog && lane == 0) blog[row] = 1;
+          if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
+          __syncwarp();
+          r += 1;
+        }
+        row_start = tstar + 1;
+        if (row_start >= tv) break;
+      }
+      if (!stopped) consumed = t0 + tv;
+    }
+    cp_wait<0>();
+    __syncwarp();
+
+    // ---- write the state back; x = x0 + C~^T W ------------------------------------
+#pragma unroll
+    for (int kt = 0; kt < IK; ++kt)
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) Cg[sigma(kt, q) * M + 8 * jt + p] = S.Cs[kt][jt][lane];
+    __syncwarp();
+    double* Dm = &S.Cs[0][0][0];  // C is written back: reuse its smem for C~, row-major [R][M]
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+      for (int J = 0; J < JK / 2; ++J) {
+        const double2 v = make_double2(Dt[nt][2 * J], Dt[nt][2 * J + 1]);
+        *reinterpret_cast<double2*>(Dg + (8 * nt + p) * M + 8 * J + 2 * q) = v;
+        *reinterpret_cast<double2*>(Dm + (8 * nt + p) * M + 8 * J + 2 * q) = v;
+      }
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt) {
+      S.u.w[8 * nt + 2 * q][p] = Wt[nt][0];
+      S.u.w[8 * nt + 2 * q + 1][p] = Wt[nt][1];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ju = 0; ju < M / 32; ++ju) {
+      const int j = lane + 32 * ju;
+      double xs[KC];
+#pragma unroll
+      for (int c = 0; c < KC; ++c) xs[c] = has_x0 ? Xg[c * M + j] : 0.0;
+      for (int i = 0; i < r; ++i) {
+        const double d = Dm[i * M + j];
+#pragma unroll
+        for (int c = 0; c < KC; ++c) xs[c] = fma(d, S.u.w[i][c], xs[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < KC; ++c) Xg[c * M + j] = xs[c];
+    }
+#pragma unroll
+    for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt)
+        *reinterpret_cast<double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q) =
+            make_double2(Pr[mt][nt][0], Pr[mt][nt][1]);
+    if (lane == 0) {
+      st.rank[b] = r;
+      st.nobs[b] = nobs0 + consumed;
+      st.status[b] = status;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace blk
+
+namespace {
+constexpr int BM = 64, BR = 16, BK = 8;
+constexpr int BWARPS = 4;
+}  // namespace
+
+bool blocked_supports(const rgb_config& cfg) {
+  return cfg.dtype == RGB_F64 && cfg.variant == RGB_GENERAL && cfg.m == BM && cfg.r_cap == BR &&
+         cfg.k == BK;
+}
+
+int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                   const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                   cudaStream_t stream, int num_sms) {
+  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;  // per-row residuals: generic kernel
+  auto kern = blk::blocked_kernel<BM, BR, BK, BWARPS>;
+  const size_t smem = sizeof(blk::WarpSmem<BM, BR, BK>) * BWARPS;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BWARPS * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t need = (cfg.num_streams + BWARPS - 1) / BWARPS;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > need) grid = need;
+  kern<<<(unsigned)grid, BWARPS * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
+                                                      (const double*)targets, tg_stride, T, logs.branch,
+                                                      (double*)logs.coords);
+  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
 }  // namespace rgb

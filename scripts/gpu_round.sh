@@ -1,5 +1,5 @@
-set -x
-free -g | head -2
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
-timeout 600 python bench.py --streams 8192 --steps 2 --warmup 1 --no-cpu 2>&1 | tail -3
+# one GPU call: tests, smoke, a bench line (inputs/logs land in gpurun_out/)
+set -o pipefail
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -4
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -25
+timeout 900 python bench.py --steps 3 --warmup 3 2>&1 | tail -3 | tee gpurun_out/bench_c5.jsonl

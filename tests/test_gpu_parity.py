@@ -217,6 +217,7 @@ def test_c5_full_length_streams_against_oracle():
     res = run_batched(rows, tg, r_cap=16)
     amb, worst = compare_to_oracle(rows, tg, res, r_cap=16)
     assert amb <= 2
+    assert worst <= 1e-11   # well inside the 1e-9 bar (blocked LDL^T keeps sequential accuracy)
     assert (res["rank"][res["status"] == 0] == 16).all()
 
 
@@ -228,6 +229,17 @@ def test_c3_full_length_streams_against_oracle():
     res = run_batched(rows, tg, r_cap=32)
     amb, worst = compare_to_oracle(rows, tg, res, r_cap=32)
     assert amb <= 1
+
+
+def test_c5_short_streams_ill_conditioned_start():
+    """256-row prefixes: the first dependent tiles see the least-conditioned
+    8x8 systems (large coordinates on a fresh 16-row basis)."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch("c5", list(range(96)), n=256)
+    res = run_batched(rows, tg, r_cap=16)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16)
+    assert amb <= 2 and worst <= 1e-11
 
 
 def test_device_generated_c5_sample_against_oracle():
@@ -247,7 +259,7 @@ def test_multi_rhs_equals_single_rhs_runs(golden):
     full = run_batched(g["rows"], g["targets"], r_cap=16, logs=False)
     for c in (0, 5):
         one = run_batched(g["rows"], g["targets"][:, :, c], r_cap=16, logs=False)
-        assert relerr(one["x"][:, :, 0], full["x"][:, :, c]) <= 1e-13
+        assert relerr(one["x"][:, :, 0], full["x"][:, :, c]) <= 1e-12
 
 
 def test_fp32_integer_streams_track_fp64(golden):
