@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librgb.so")
+# RGB_LIB_PATH selects an alternative build of the same library (tuning A/B runs)
+LIB_PATH = os.environ.get("RGB_LIB_PATH") or os.path.join(HERE, "librgb.so")
 
 RGB_ABI_VERSION = 1
 F64, F32 = 0, 1

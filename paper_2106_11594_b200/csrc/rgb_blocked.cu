@@ -70,6 +70,17 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 __device__ __forceinline__ int sigma(int kt, int q) { return 8 * (kt >> 1) + 2 * q + (kt & 1); }
 
+// 1/x to within an ulp without branches: MUFU.RCP64H seed (rcp.approx.ftz.f64)
+// and two Newton steps.  Only used for LDL^T pivots of I + G P G^T (>= 1).
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <int M, int R, int KC>
 struct WarpSmem {
   double Cs[R / 4][M / 8][32];   // basis C as the B operand of R = A - G C
@@ -85,8 +96,12 @@ struct WarpSmem {
   } u;
 };
 
+#ifndef RGB_BLOCKED_MINB
+#define RGB_BLOCKED_MINB 3
+#endif
+
 template <int M, int R, int KC, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) blocked_kernel(
+__global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
     const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
     double* __restrict__ clog) {
@@ -147,303 +162,421 @@ __global__ void __launch_bounds__(WARPS * 32) blocked_kernel(
     const bool has_x0 = __any_sync(FULL, nz);
     __syncwarp();
 
-    // ---- tile loop ----------------------------------------------------------------
+    // ---- tile loop -----------------------------------------------------------------
+    // front(i): coords, rejections and the rank test of tile i (tensor cores);
+    // scan(i):  the blocked Sherman-Morrison update of its dependent rows.
+    // When tile i is all dependent the basis does not move, so front(i+1) is
+    // issued together with scan(i) and the two overlap (no speculation).
     const int64_t ntiles = (T + TT - 1) / TT;
     int64_t consumed = 0;
     auto prefetch = [&](int64_t tile, int s) {
-      const int64_t t0 = tile * TT;
-      const int64_t t = t0 + p;
-      const bool ok = t < T;
-      const double* src = ok ? Rb + t * M : Rb;
+      if (tile < ntiles) {
+        const int64_t t0 = tile * TT;
+        const int64_t t = t0 + p;
+        const bool ok = t < T;
+        const double* src = ok ? Rb + t * M : Rb;
 #pragma unroll
-      for (int nt = 0; nt < JT; ++nt) cp_async16(&S.At[s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
+        for (int nt = 0; nt < JT; ++nt) cp_async16(&S.At[s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t ty = t0 + 2 * q + e;
-        const bool oky = ty < T;
-        cp_async8(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky ? 8 : 0);
+        for (int e = 0; e < 2; ++e) {
+          const int64_t ty = t0 + 2 * q + e;
+          const bool oky = ty < T;
+          cp_async8(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky ? 8 : 0);
+        }
       }
       cp_commit();
     };
-    if (ntiles > 0) prefetch(0, 0);
-    bool stopped = false;
-    for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
-      const int s = (int)(tile & 1);
-      if (tile + 1 < ntiles) {
-        prefetch(tile + 1, s ^ 1);
-        cp_wait<1>();
-      } else {
-        cp_wait<0>();
-      }
-      double a[JT][2];
+
+    struct Front {
+      double g[IT][2];   // G[t=p][8nt+2q+e]
+      double rsq, asq;   // |rej_t|^2, |a_t|^2 for t = p
+      double dyx[2];     // y - a.x0 for (c = p, t = 2q+e)
+      unsigned badm;     // rows with non-finite input (bit 4t)
+      int tstar, tv;     // first stopping row (tv if none), valid rows
+      int64_t t0;
+    };
+    // front pieces: the projection of one tile, split so that the fast path
+    // can interleave it with the previous tile's scan (the scheduler keeps
+    // source order for these long chains, so the interleave is written out).
+    struct FrontAcc {
+      double g2[IT][2];   // second K-half of G (two chains per N tile)
+      double acc[JT][2];  // G C
+    };
+    auto front_begin = [&](int64_t tile, int s, Front& F, FrontAcc& X) {
+      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+      F.t0 = tile * TT;
+      F.tv = (int)((T - F.t0) < TT ? (T - F.t0) : TT);
+      const double2 yy = *reinterpret_cast<const double2*>(&S.Yt[s][lane][0]);
+      F.dyx[0] = yy.x;
+      F.dyx[1] = yy.y;
+      // row norms |a_t|^2 (solver.py:267)
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int nt = 0; nt < JT; ++nt) {
-        double2 v = *reinterpret_cast<const double2*>(&S.At[s][nt][lane][0]);
-        a[nt][0] = v.x;
-        a[nt][1] = v.y;
+        const double2 v = As[nt * 32];
+        s4[(2 * nt) & 3] = fma(v.x, v.x, s4[(2 * nt) & 3]);
+        s4[(2 * nt + 1) & 3] = fma(v.y, v.y, s4[(2 * nt + 1) & 3]);
       }
-      double yv[2];
-      {
-        double2 v = *reinterpret_cast<const double2*>(&S.Yt[s][lane][0]);
-        yv[0] = v.x;
-        yv[1] = v.y;
-      }
-      const int64_t t0 = tile * TT;
-      const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
-
-      // row norms |a_t|^2 (solver.py:267), quad-reduced: all 4 lanes of row p
-      double asq = 0.0;
+      F.asq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
-      for (int nt = 0; nt < JT; ++nt) asq = fma(a[nt][0], a[nt][0], fma(a[nt][1], a[nt][1], asq));
+      for (int nt = 0; nt < IT; ++nt) F.g[nt][0] = F.g[nt][1] = X.g2[nt][0] = X.g2[nt][1] = 0.0;
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) X.acc[jt][0] = X.acc[jt][1] = 0.0;
+    };
+    // G = A C~^T (M = t, N = i, K = j; solver.py:286): K steps 2J, 2J + 1
+    auto front_g1 = [&](int s, int J, Front& F, FrontAcc& X) {
+      const double2 v = reinterpret_cast<const double2*>(&S.At[s][0][lane][0])[J * 32];
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        mma(F.g[nt], v.x, Dt[nt][2 * J]);
+        mma(X.g2[nt], v.y, Dt[nt][2 * J + 1]);
+      }
+      if (J == JK / 2 - 1) {
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          F.g[nt][0] += X.g2[nt][0];
+          F.g[nt][1] += X.g2[nt][1];
+        }
+      }
+    };
+    // G C (M = t, N = j, K = i; solver.py:287): K step kt
+    auto front_g2 = [&](int kt, Front& F, FrontAcc& X) {
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) mma(X.acc[jt], F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+    };
+    // |R_t|^2 = |a_t - (G C)_t|^2 and the rank test (solver.py:288-296)
+    auto front_end = [&](int s, int row_start, Front& F, FrontAcc& X) {
+      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) {
+        const double2 v = As[jt * 32];
+        const double r0 = v.x - X.acc[jt][0], r1 = v.y - X.acc[jt][1];
+        s4[(2 * jt) & 3] = fma(r0, r0, s4[(2 * jt) & 3]);
+        s4[(2 * jt + 1) & 3] = fma(r1, r1, s4[(2 * jt + 1) & 3]);
+      }
+      double rsq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      double asq = F.asq;
       asq += __shfl_xor_sync(FULL, asq, 1);
+      rsq += __shfl_xor_sync(FULL, rsq, 1);
       asq += __shfl_xor_sync(FULL, asq, 2);
-      // non-finite targets, per row (scalars.py:122-123 rejects them)
-      const unsigned yb0 = __ballot_sync(FULL, !isfinite(yv[0]));
-      const unsigned yb1 = __ballot_sync(FULL, !isfinite(yv[1]));
+      rsq += __shfl_xor_sync(FULL, rsq, 2);
+      F.asq = asq;
+      F.rsq = rsq;
+      // rank test with the current rank; NaN/Inf rows stop the stream
+      const unsigned yb0 = __ballot_sync(FULL, !isfinite(F.dyx[0]));
+      const unsigned yb1 = __ballot_sync(FULL, !isfinite(F.dyx[1]));
       const bool ybad = (((p & 1) ? yb1 : yb0) & (0x11111111u << (p >> 1))) != 0u;
-      // dyx = y - a.x0 for (c = p, t = 2q + e)
-      double dyx[2] = {yv[0], yv[1]};
+      const bool valid = p >= row_start && p < F.tv;
+      const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
+      const bool bad = !isfinite(asq) || ybad;
+      const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
+      F.badm = __ballot_sync(FULL, q == 0 && valid && bad);
+      F.tstar = stopm ? (__ffs(stopm) - 1) >> 2 : F.tv;
+    };
+    auto front = [&](int64_t tile, int s, int row_start, Front& F) {
+      FrontAcc X;
+      front_begin(tile, s, F, X);
+#pragma unroll
+      for (int J = 0; J < JK / 2; ++J) front_g1(s, J, F, X);
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) front_g2(kt, F, X);
+      front_end(s, row_start, F, X);
+    };
+    // a.x0 for a stream that did not start empty: Y0^T = x0^T A^T (M = c, N = t, K = j)
+    auto front_x0 = [&](int s, Front& F) {
       if (has_x0) {
+        const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int J = 0; J < JK / 2; ++J) {
-          double2 xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q));
-          mma(acc, xv.x, a[J][0]);
-          mma(acc, xv.y, a[J][1]);
+          const double2 xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q));
+          const double2 v = As[J * 32];
+          mma(acc, xv.x, v.x);
+          mma(acc, xv.y, v.y);
         }
-        dyx[0] -= acc[0];
-        dyx[1] -= acc[1];
+        F.dyx[0] -= acc[0];
+        F.dyx[1] -= acc[1];
       }
+    };
 
-      int row_start = 0;
-      while (true) {
-        // G = A C~^T : M = t, N = i, K = j
-        double g[IT][2], g2[IT][2];
+    // scan pieces: blocked Sherman-Morrison over the dependent rows [rs, te)
+    struct ScanWork {
+      double gm[IT][2], dy[2], u[IT][2], mi[2], ev[2];
+    };
+    auto scan_a = [&](const Front& F, int rs, int te, ScanWork& X) {
+      const bool inb = p >= rs && p < te;
 #pragma unroll
-        for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = g2[nt][0] = g2[nt][1] = 0.0;
+      for (int nt = 0; nt < IT; ++nt) {
+        X.gm[nt][0] = inb ? F.g[nt][0] : 0.0;
+        X.gm[nt][1] = inb ? F.g[nt][1] : 0.0;
+      }
+      // dy0^T = dyx - (G W)^T : M = c, N = t, K = i  (a-priori residuals, solver.py:303)
+      {
+        double acc[2] = {0.0, 0.0};
 #pragma unroll
-        for (int kt = 0; kt < JK; kt += 2)
+        for (int kt = 0; kt < IK; ++kt) mma(acc, Wt[kt >> 1][kt & 1], X.gm[kt >> 1][kt & 1]);
 #pragma unroll
-          for (int nt = 0; nt < IT; ++nt) {
-            mma(g[nt], a[kt >> 1][0], Dt[nt][kt]);
-            mma(g2[nt], a[kt >> 1][1], Dt[nt][kt + 1]);
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int t = 2 * q + e;
+          X.dy[e] = (t >= rs && t < te) ? F.dyx[e] - acc[e] : 0.0;
+        }
+      }
+      // U^T = G P (M = t, N = i); U = (U^T)^T by quad-crossing shuffles
+      double ut[IT][2];
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        ut[nt][0] = ut[nt][1] = 0.0;
+#pragma unroll
+        for (int kt = 0; kt < IK; ++kt) mma(ut[nt], X.gm[kt >> 1][kt & 1], Pr[nt][kt >> 1][kt & 1]);
+      }
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int src = 4 * (2 * q + e) + (p >> 1);
+          const double v0 = __shfl_sync(FULL, ut[mt][0], src);
+          const double v1 = __shfl_sync(FULL, ut[mt][1], src);
+          X.u[mt][e] = (p & 1) ? v1 : v0;
+        }
+      // M = I + G P G^T (M = t, N = t')
+      X.mi[0] = X.mi[1] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) mma(X.mi, ut[kt >> 1][kt & 1], X.gm[kt >> 1][kt & 1]);
+      if (p == 2 * q) X.mi[0] += 1.0;
+      if (p == 2 * q + 1) X.mi[1] += 1.0;
+      X.ev[0] = p == 2 * q ? 1.0 : 0.0;
+      X.ev[1] = p == 2 * q + 1 ? 1.0 : 0.0;
+    };
+    // M = L diag(d) L^T by forward elimination on [M | I]: E = L^-1 (unit
+    // lower), d = pivots -- the 8 sequential Sherman-Morrison steps of
+    // solver.py:298-301 in factored form (an explicit M^-1 / Woodbury update
+    // loses accuracy when M is ill-conditioned; the factored form does not)
+    auto scan_elim = [&](int k, ScanWork& X) {
+      const double v = (k & 1) ? X.mi[1] : X.mi[0];
+      const double piv = __shfl_sync(FULL, v, 4 * k + (k >> 1));
+      const double mps = __shfl_sync(FULL, v, 4 * p + (k >> 1));
+      const double m0 = __shfl_sync(FULL, X.mi[0], 4 * k + q);
+      const double m1 = __shfl_sync(FULL, X.mi[1], 4 * k + q);
+      const double e0 = __shfl_sync(FULL, X.ev[0], 4 * k + q);
+      const double e1 = __shfl_sync(FULL, X.ev[1], 4 * k + q);
+      const double f = (p > k) ? mps * rcp64(piv) : 0.0;
+      X.mi[0] = fma(-f, m0, X.mi[0]);
+      X.mi[1] = fma(-f, m1, X.mi[1]);
+      X.ev[0] = fma(-f, e0, X.ev[0]);
+      X.ev[1] = fma(-f, e1, X.ev[1]);
+    };
+    struct ScanTail {
+      double rd0, rd1, yt[IT][2], dh[2];
+    };
+    // 1/d_t for t = 2q, 2q + 1;  Y^T = U E^T (columns = the z_t of the sequential form)
+    auto scan_b1 = [&](ScanWork& X, ScanTail& Z) {
+      const double dsel = (p & 1) ? X.mi[1] : X.mi[0];
+      const double rd = rcp64(__shfl_sync(FULL, dsel, 4 * p + (p >> 1)));
+      Z.rd0 = __shfl_sync(FULL, rd, 8 * q);
+      Z.rd1 = __shfl_sync(FULL, rd, 8 * q + 4);
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt) {
+        Z.yt[mt][0] = Z.yt[mt][1] = 0.0;
+        mma(Z.yt[mt], X.u[mt][0], X.ev[0]);
+        mma(Z.yt[mt], X.u[mt][1], X.ev[1]);
+      }
+      // E dy0 (M = c, N = t, K = t'): the residuals the sequential form would see
+      Z.dh[0] = Z.dh[1] = 0.0;
+      mma(Z.dh, X.dy[0], X.ev[0]);
+      mma(Z.dh, X.dy[1], X.ev[1]);
+    };
+    // P -= Y^T D^-1 Y   and   W^T += (E dy0)^T D^-1 Y   (solver.py:300-304)
+    auto scan_b2 = [&](ScanTail& Z) {
+      const double d0 = Z.dh[0] * Z.rd0, d1 = Z.dh[1] * Z.rd1;
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt) {
+        const double s0 = -Z.yt[mt][0] * Z.rd0, s1 = -Z.yt[mt][1] * Z.rd1;
 #pragma unroll
         for (int nt = 0; nt < IT; ++nt) {
-          g[nt][0] += g2[nt][0];
-          g[nt][1] += g2[nt][1];
+          mma(Pr[mt][nt], s0, Z.yt[nt][0]);
+          mma(Pr[mt][nt], s1, Z.yt[nt][1]);
         }
-        // R = A - G C and |R_t|^2 : M = t, N = j, K = i
-        double rsq = 0.0;
+      }
 #pragma unroll
-        for (int jt = 0; jt < JT; ++jt) {
-          double acc[2] = {0.0, 0.0};
+      for (int nt = 0; nt < IT; ++nt) {
+        mma(Wt[nt], d0, Z.yt[nt][0]);
+        mma(Wt[nt], d1, Z.yt[nt][1]);
+      }
+    };
+    auto scan = [&](const Front& F, int rs, int te) {
+      ScanWork X;
+      ScanTail Z;
+      scan_a(F, rs, te, X);
 #pragma unroll
-          for (int kt = 0; kt < IK; ++kt) mma(acc, g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
-          const double r0 = a[jt][0] - acc[0], r1 = a[jt][1] - acc[1];
-          rsq = fma(r0, r0, fma(r1, r1, rsq));
-        }
-        rsq += __shfl_xor_sync(FULL, rsq, 1);
-        rsq += __shfl_xor_sync(FULL, rsq, 2);
-        // rank test per row with the current rank
-        const double esq = eps_sq<double>(cfg, r);
-        const bool valid = p >= row_start && p < tv;
-        const bool dep = is_dependent<double>(rsq, asq, esq);
-        const bool bad = !isfinite(asq) || ybad;
-        const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
-        const unsigned badm = __ballot_sync(FULL, q == 0 && valid && bad);
-        const int tstar = stopm ? (__ffs(stopm) - 1) >> 2 : tv;
+      for (int k = 0; k < TT - 1; ++k) scan_elim(k, X);
+      scan_b1(X, Z);
+      scan_b2(Z);
+    };
+    // scan(tile i) with front(tile i+1) written out interleaved (fast path)
+    auto scan_front = [&](const Front& F, int64_t tile_n, int s_n, Front& N) {
+      ScanWork X;
+      ScanTail Z;
+      FrontAcc A;
+      front_begin(tile_n, s_n, N, A);
+      scan_a(F, 0, F.tv, X);
+      front_g1(s_n, 0, N, A);
+      front_g1(s_n, 1, N, A);
+#pragma unroll
+      for (int k = 0; k < TT - 1; ++k) {
+        scan_elim(k, X);
+        if (k + 2 < JK / 2) front_g1(s_n, k + 2, N, A);
+        else front_g2(k + 2 - JK / 2, N, A);
+      }
+      scan_b1(X, Z);
+      front_g2(IK - 3, N, A);
+      front_g2(IK - 2, N, A);
+      scan_b2(Z);
+      front_g2(IK - 1, N, A);
+      front_end(s_n, 0, N, A);
+    };
 
-        if (tstar > row_start) {
-          // ---- dependent rows [row_start, tstar): blocked Sherman-Morrison --------
-          const bool inb = p >= row_start && p < tstar;
-          double gm[IT][2];
+    // logs of dependent rows [rs, te): branch 0 and the coordinate row gamma_t
+    // (zero beyond the rank).  Kept out of scan() so that scan and the next
+    // front form one branch-free block the scheduler can interleave.
+    auto log_dependent = [&](const Front& F, int rs, int te) {
+      if (blog || clog) {
+        if (p >= rs && p < te) {
+          const int64_t row = b * T + F.t0 + p;
+          if (blog && q == 0) blog[row] = 0;
+          if (clog) {
 #pragma unroll
-          for (int nt = 0; nt < IT; ++nt) {
-            gm[nt][0] = inb ? g[nt][0] : 0.0;
-            gm[nt][1] = inb ? g[nt][1] : 0.0;
-          }
-          // dy0^T = dyx - (G W)^T : M = c, N = t, K = i
-          double dy[2];
-          {
-            double acc[2] = {0.0, 0.0};
-#pragma unroll
-            for (int kt = 0; kt < IK; ++kt) mma(acc, Wt[kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int t = 2 * q + e;
-              dy[e] = (t >= row_start && t < tstar) ? dyx[e] - acc[e] : 0.0;
-            }
-          }
-          // U = P G^T (M = i, N = t) and U^T = G P (M = t, N = i)
-          double u[IT][2], ut[IT][2];
-#pragma unroll
-          for (int mt = 0; mt < IT; ++mt) {
-            u[mt][0] = u[mt][1] = ut[mt][0] = ut[mt][1] = 0.0;
-#pragma unroll
-            for (int kt = 0; kt < IK; ++kt) {
-              mma(u[mt], Pr[mt][kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
-              mma(ut[mt], gm[kt >> 1][kt & 1], Pr[mt][kt >> 1][kt & 1]);
-            }
-          }
-          // M = I + G P G^T  (8 x 8, M = t, N = t')
-          double mi[2] = {0.0, 0.0};
-#pragma unroll
-          for (int kt = 0; kt < IK; ++kt) mma(mi, ut[kt >> 1][kt & 1], gm[kt >> 1][kt & 1]);
-          if (p == 2 * q) mi[0] += 1.0;
-          if (p == 2 * q + 1) mi[1] += 1.0;
-          // M = L diag(d) L^T by forward elimination on [M | I]: E = L^-1
-          // (unit lower), d = pivots.  This is the 8-step Sherman-Morrison
-          // recursion in factored form: z_t = (U E^T)_t / d_t exactly as the
-          // sequential steps of solver.py:298-301 (an explicit M^-1 loses
-          // accuracy when M is ill-conditioned; the factored form does not).
-          double ev[2] = {p == 2 * q ? 1.0 : 0.0, p == 2 * q + 1 ? 1.0 : 0.0};
-#pragma unroll
-          for (int k = 0; k < TT - 1; ++k) {
-            const double v = (k & 1) ? mi[1] : mi[0];
-            const double piv = __shfl_sync(FULL, v, 4 * k + (k >> 1));
-            const double mps = __shfl_sync(FULL, v, 4 * p + (k >> 1));
-            const double m0 = __shfl_sync(FULL, mi[0], 4 * k + q);
-            const double m1 = __shfl_sync(FULL, mi[1], 4 * k + q);
-            const double e0 = __shfl_sync(FULL, ev[0], 4 * k + q);
-            const double e1 = __shfl_sync(FULL, ev[1], 4 * k + q);
-            if (p > k) {
-              const double f = mps / piv;
-              mi[0] = fma(-f, m0, mi[0]);
-              mi[1] = fma(-f, m1, mi[1]);
-              ev[0] = fma(-f, e0, ev[0]);
-              ev[1] = fma(-f, e1, ev[1]);
-            }
-          }
-          // 1/d_t for t = p (quad-shared) and for t = 2q, 2q + 1
-          const double dsel = (p & 1) ? mi[1] : mi[0];
-          const double rd = 1.0 / __shfl_sync(FULL, dsel, 4 * p + (p >> 1));
-          const double rd0 = __shfl_sync(FULL, rd, 8 * q);
-          const double rd1 = __shfl_sync(FULL, rd, 8 * q + 4);
-          // Y^T = U E^T (M = i, N = t, K = t'): column t is z_t of the sequential form
-          double yt[IT][2];
-#pragma unroll
-          for (int mt = 0; mt < IT; ++mt) {
-            yt[mt][0] = yt[mt][1] = 0.0;
-            mma(yt[mt], u[mt][0], ev[0]);
-            mma(yt[mt], u[mt][1], ev[1]);
-          }
-          // E dy0 (M = c, N = t, K = t'): the a-priori residuals of the 8 rows
-          double dh[2] = {0.0, 0.0};
-          mma(dh, dy[0], ev[0]);
-          mma(dh, dy[1], ev[1]);
-          dh[0] *= rd0;
-          dh[1] *= rd1;
-          // P -= Y^T D^-1 Y   and   W^T += (E dy0)^T D^-1 Y
-#pragma unroll
-          for (int mt = 0; mt < IT; ++mt) {
-            const double s0 = -yt[mt][0] * rd0, s1 = -yt[mt][1] * rd1;
-#pragma unroll
-            for (int nt = 0; nt < IT; ++nt) {
-              mma(Pr[mt][nt], s0, yt[nt][0]);
-              mma(Pr[mt][nt], s1, yt[nt][1]);
-            }
-          }
-#pragma unroll
-          for (int nt = 0; nt < IT; ++nt) {
-            mma(Wt[nt], dh[0], yt[nt][0]);
-            mma(Wt[nt], dh[1], yt[nt][1]);
-          }
-          // logs: branch 0, coordinate row gamma_t (zero beyond the rank)
-          if (inb) {
-            const int64_t row = b * T + t0 + p;
-            if (blog && q == 0) blog[row] = 0;
-            if (clog) {
-#pragma unroll
-              for (int nt = 0; nt < IT; ++nt)
-                *reinterpret_cast<double2*>(clog + row * R + 8 * nt + 2 * q) = make_double2(g[nt][0], g[nt][1]);
-            }
+            for (int nt = 0; nt < IT; ++nt)
+              *reinterpret_cast<double2*>(clog + row * R + 8 * nt + 2 * q) = make_double2(F.g[nt][0], F.g[nt][1]);
           }
         }
-        if (tstar >= tv) break;
+      }
+    };
 
-        // ---- row tstar: non-finite input or rank growth ------------------------------
-        if ((badm >> (4 * tstar)) & 1u) {
+    // independent row ts of front F (solver.py:305-318, _grow solver.py:368-397)
+    auto grow = [&](const Front& F, int s, int ts) {
+      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+      const double rs = __shfl_sync(FULL, F.rsq, 4 * ts);
+      if (p == ts) {
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          S.u.ind.gam[8 * nt + 2 * q] = F.g[nt][0];
+          S.u.ind.gam[8 * nt + 2 * q + 1] = F.g[nt][1];
+        }
+      }
+      // the rejection of row ts on the current basis, recomputed (rare path)
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) {
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kt = 0; kt < IK; ++kt) mma(acc, F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+        if (p == ts) {
+          const double2 v = As[jt * 32];
+          S.u.ind.kv[8 * jt + 2 * q] = (v.x - acc[0]) / rs;       // K = rej / |rej|^2
+          S.u.ind.kv[8 * jt + 2 * q + 1] = (v.y - acc[1]) / rs;
+          S.u.ind.av[8 * jt + 2 * q] = v.x;
+          S.u.ind.av[8 * jt + 2 * q + 1] = v.y;
+        }
+      }
+      __syncwarp();
+      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
+      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
+      const double wnew = __shfl_sync(FULL, dv, 4 * p + (ts >> 1));
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (8 * nt + 2 * q + e == r) Wt[nt][e] = wnew;
+      // C~[:r] -= gamma K^T, C~[r] = K   (solver.py:377-380)
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        const int i = 8 * nt + p;
+        const double gi = S.u.ind.gam[i];
+#pragma unroll
+        for (int J = 0; J < JK / 2; ++J) {
+          const double2 kv = *reinterpret_cast<const double2*>(&S.u.ind.kv[8 * J + 2 * q]);
+          Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
+          Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
+        }
+      }
+      // C[r] = a  (solver.py:376)
+      if (q == ((r & 7) >> 1)) {
+        const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = S.u.ind.av[8 * jt + p];
+      }
+      // P = diag(P, 1)  (solver.py:372-373, 381)
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
+            if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
+          }
+      const int64_t row = b * T + F.t0 + ts;
+      if (blog && lane == 0) blog[row] = 1;
+      if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
+      __syncwarp();
+      r += 1;
+    };
+
+    bool stopped = false;
+    Front F;
+    if (ntiles > 0) {
+      prefetch(0, 0);
+      prefetch(1, 1);
+      cp_wait<1>();
+      front(0, 0, 0, F);
+      front_x0(0, F);
+    }
+    for (int64_t tile = 0; tile < ntiles; ++tile) {
+      const int s = (int)(tile & 1);
+      if (F.tstar >= F.tv) {
+        // every row of the tile is dependent: scan(i) overlaps front(i+1)
+        prefetch(tile + 2, s);
+        cp_wait<1>();
+        Front N;
+        scan_front(F, tile + 1, s ^ 1, N);
+        log_dependent(F, 0, F.tv);
+        front_x0(s ^ 1, N);
+        consumed = F.t0 + F.tv;
+        F = N;
+        continue;
+      }
+      int row_start = 0;
+      while (true) {
+        if (F.tstar > row_start) {
+          scan(F, row_start, F.tstar);
+          log_dependent(F, row_start, F.tstar);
+        }
+        if (F.tstar >= F.tv) break;
+        if ((F.badm >> (4 * F.tstar)) & 1u) {
           status |= RGB_ST_NONFINITE;
-          consumed = t0 + tstar;
           stopped = true;
           break;
         }
         if (r >= R) {
           status |= RGB_ST_RANK_CAP;
-          consumed = t0 + tstar;
           stopped = true;
           break;
         }
-        {
-          // rejection of row tstar on the current basis (recomputed: rare path)
-          const double rs = __shfl_sync(FULL, rsq, 4 * tstar);
-          if (p == tstar) {
-#pragma unroll
-            for (int nt = 0; nt < IT; ++nt) {
-              S.u.ind.gam[8 * nt + 2 * q] = g[nt][0];
-              S.u.ind.gam[8 * nt + 2 * q + 1] = g[nt][1];
-            }
-          }
-#pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
-            double acc[2] = {0.0, 0.0};
-#pragma unroll
-            for (int kt = 0; kt < IK; ++kt) mma(acc, g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
-            if (p == tstar) {
-              S.u.ind.kv[8 * jt + 2 * q] = (a[jt][0] - acc[0]) / rs;
-              S.u.ind.kv[8 * jt + 2 * q + 1] = (a[jt][1] - acc[1]) / rs;
-              S.u.ind.av[8 * jt + 2 * q] = a[jt][0];
-              S.u.ind.av[8 * jt + 2 * q + 1] = a[jt][1];
-            }
-          }
-          __syncwarp();
-          // W gains row r: y - a.x0 of row tstar (x = x0 + C~^T W stays exact)
-          const double dv = (tstar & 1) ? dyx[1] : dyx[0];
-          const double wnew = __shfl_sync(FULL, dv, 4 * p + (tstar >> 1));
-#pragma unroll
-          for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              if (8 * nt + 2 * q + e == r) Wt[nt][e] = wnew;
-          // C~[:r] -= gamma K^T, C~[r] = K   (solver.py:377-380)
-#pragma unroll
-          for (int nt = 0; nt < IT; ++nt) {
-            const int i = 8 * nt + p;
-            const double gi = S.u.ind.gam[i];
-#pragma unroll
-            for (int J = 0; J < JK / 2; ++J) {
-              const double2 kv = *reinterpret_cast<const double2*>(&S.u.ind.kv[8 * J + 2 * q]);
-              Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
-              Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
-            }
-          }
-          // C[r] = a  (solver.py:376)
-          if (q == ((r & 7) >> 1)) {
-            const int ktr = 2 * (r >> 3) + (r & 1);
-#pragma unroll
-            for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = S.u.ind.av[8 * jt + p];
-          }
-          // P = diag(P, 1)  (solver.py:372-373, 381)
-#pragma unroll
-          for (int mt = 0; mt < IT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
-                if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
-              }
-          const int64_t row = b * T + t0 + tstar;
-          if (blog && lane == 0) blog[row] = 1;
-          if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
-          __syncwarp();
-          r += 1;
-        }
-        row_start = tstar + 1;
-        if (row_start >= tv) break;
+        grow(F, s, F.tstar);
+        row_start = F.tstar + 1;
+        if (row_start >= F.tv) break;
+        front(tile, s, row_start, F);   // re-project the rest of the tile on the new basis
+        front_x0(s, F);
       }
-      if (!stopped) consumed = t0 + tv;
+      if (stopped) {
+        consumed = F.t0 + F.tstar;
+        break;
+      }
+      consumed = F.t0 + F.tv;
+      prefetch(tile + 2, s);
+      cp_wait<1>();
+      front(tile + 1, s ^ 1, 0, F);
+      front_x0(s ^ 1, F);
     }
     cp_wait<0>();
     __syncwarp();
@@ -502,7 +635,10 @@ __global__ void __launch_bounds__(WARPS * 32) blocked_kernel(
 
 namespace {
 constexpr int BM = 64, BR = 16, BK = 8;
-constexpr int BWARPS = 4;
+#ifndef RGB_BLOCKED_WARPS
+#define RGB_BLOCKED_WARPS 4
+#endif
+constexpr int BWARPS = RGB_BLOCKED_WARPS;
 }  // namespace
 
 bool blocked_supports(const rgb_config& cfg) {
