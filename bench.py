@@ -44,7 +44,7 @@ UNIT = "rows*streams/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c5", choices=sorted(workloads.CONFIGS))
@@ -88,11 +88,11 @@ def alg_bytes(S, n, m, k, s):
 # -- clocks ------------------------------------------------------------------------
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,timestamp")
 
     def __init__(self, index):
         self.index = index
@@ -105,9 +105,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        # wait for the first sample so that the timed region is covered
+        t0 = time.time()
+        while time.time() - t0 < 5 and os.path.getsize(self.path) == 0:
+            time.sleep(0.05)
 
     def stop(self):
         if self.proc is None:
@@ -353,6 +358,17 @@ def run_ours(args):
         parity = {"streams": ns, "rank_match": bool(np.array_equal(ranks[:ns][ok], o["rank"][ok])),
                   "x_relerr_max": max(errs) if errs else None,
                   "tolerance": 1e-9 if args.dtype == "fp64" else 1e-3}
+        # streams the device froze at the rank capacity: the oracle, given room
+        # to grow, must run away past the construction rank too (SURVEY.md
+        # finding 0.3: the reference itself does on ~1 in 2048 C5 streams)
+        capped = np.nonzero(status & 1)[0][:6]
+        if len(capped):
+            rc_ = torch.tensor(capped, device=device, dtype=torch.long)
+            o2 = oracle.ingest(rows[rc_].cpu().numpy().astype(np.float64), tg[rc_].cpu().numpy().astype(np.float64),
+                               r_cap=n, nthreads=8, logs=False)
+            parity["rank_cap_streams_checked"] = int(len(capped))
+            parity["rank_cap_oracle_ranks"] = [int(v) for v in o2["rank"]]
+            parity["rank_cap_oracle_runaway"] = bool((o2["rank"] > cfg.r).all())
 
     # end-to-end through the public API from pinned host buffers
     e2e = None

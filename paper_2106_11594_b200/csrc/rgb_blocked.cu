@@ -92,8 +92,9 @@ struct WarpSmem {
       double kv[M];              // its gain K = rej / |rej|^2
       double av[M];              // the row itself
     } ind;
-    double w[R][KC];             // W at the end of the call
   } u;
+  // at the end of a call C~ is staged row-major with stride M + 2 over Cs and At
+  static_assert(sizeof(Cs) + sizeof(At) >= sizeof(double) * R * (M + 2), "staging");
 };
 
 #ifndef RGB_BLOCKED_MINB
@@ -126,38 +127,44 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     const double* Yb = tgts + b * tstride;
 
     // ---- load the stream's state into fragment layouts -------------------------
+    // A rank-0 stream is all zeros by the state contract (include/rgb.h: rows
+    // beyond the rank are zero, and the minimum-norm solution of rank 0 is 0),
+    // so a fresh solve reads nothing.
+    const bool fresh = (r == 0);
     double Dt[IT][JK];
+    double Pr[IT][IT][2];
+    double Wt[IT][2];
 #pragma unroll
-    for (int nt = 0; nt < IT; ++nt)
+    for (int nt = 0; nt < IT; ++nt) {
+      Wt[nt][0] = Wt[nt][1] = 0.0;
 #pragma unroll
       for (int J = 0; J < JK / 2; ++J) {
-        double2 v = *reinterpret_cast<const double2*>(Dg + (8 * nt + p) * M + 8 * J + 2 * q);
+        const double2 v = fresh ? make_double2(0.0, 0.0)
+                                : *reinterpret_cast<const double2*>(Dg + (8 * nt + p) * M + 8 * J + 2 * q);
         Dt[nt][2 * J] = v.x;
         Dt[nt][2 * J + 1] = v.y;
       }
-    double Pr[IT][IT][2];
 #pragma unroll
-    for (int mt = 0; mt < IT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt) {
-        double2 v = *reinterpret_cast<const double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q);
-        Pr[mt][nt][0] = v.x;
-        Pr[mt][nt][1] = v.y;
+      for (int mt = 0; mt < IT; ++mt) {
+        const double2 v = fresh ? make_double2(0.0, 0.0)
+                                : *reinterpret_cast<const double2*>(Pg + (8 * nt + p) * R + 8 * mt + 2 * q);
+        Pr[nt][mt][0] = v.x;
+        Pr[nt][mt][1] = v.y;
       }
+    }
 #pragma unroll
     for (int kt = 0; kt < IK; ++kt)
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) S.Cs[kt][jt][lane] = Cg[sigma(kt, q) * M + 8 * jt + p];
-    double Wt[IT][2];
-#pragma unroll
-    for (int nt = 0; nt < IT; ++nt) Wt[nt][0] = Wt[nt][1] = 0.0;
-    // x0 = the solution at call start; when it is exactly zero (a fresh
-    // stream) a.x0 = 0 and its contraction is skipped.
+      for (int jt = 0; jt < JT; ++jt) S.Cs[kt][jt][lane] = fresh ? 0.0 : Cg[sigma(kt, q) * M + 8 * jt + p];
+    // x0 = the solution at call start; when it is exactly zero a.x0 = 0 and
+    // its contraction is skipped.
     bool nz = false;
+    if (!fresh) {
 #pragma unroll
-    for (int J = 0; J < JK / 2; ++J) {
-      double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q);
-      nz |= (v.x != 0.0) || (v.y != 0.0);
+      for (int J = 0; J < JK / 2; ++J) {
+        double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q);
+        nz |= (v.x != 0.0) || (v.y != 0.0);
+      }
     }
     const bool has_x0 = __any_sync(FULL, nz);
     __syncwarp();
@@ -464,18 +471,28 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           S.u.ind.gam[8 * nt + 2 * q + 1] = F.g[nt][1];
         }
       }
-      // the rejection of row ts on the current basis, recomputed (rare path)
+      // the rejection of row ts on the current basis, recomputed (rare path;
+      // rows of C beyond the rank are zero, so only ceil(r/8) K pairs matter)
+      {
+        double acc[JT][2];
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) {
-        double acc[2] = {0.0, 0.0};
+        for (int jt = 0; jt < JT; ++jt) acc[jt][0] = acc[jt][1] = 0.0;
 #pragma unroll
-        for (int kt = 0; kt < IK; ++kt) mma(acc, F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+        for (int kt = 0; kt < IK; ++kt) {
+          if (kt >= 2 && r <= 8) break;
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) mma(acc[jt], F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
+        }
+        // K = rej / |rej|^2 (solver.py:336); one rounding more than a division
+        const double rinv = 1.0 / rs;
         if (p == ts) {
-          const double2 v = As[jt * 32];
-          S.u.ind.kv[8 * jt + 2 * q] = (v.x - acc[0]) / rs;       // K = rej / |rej|^2
-          S.u.ind.kv[8 * jt + 2 * q + 1] = (v.y - acc[1]) / rs;
-          S.u.ind.av[8 * jt + 2 * q] = v.x;
-          S.u.ind.av[8 * jt + 2 * q + 1] = v.y;
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double2 v = As[jt * 32];
+            *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
+                make_double2((v.x - acc[jt][0]) * rinv, (v.y - acc[jt][1]) * rinv);
+            *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) = v;
+          }
         }
       }
       __syncwarp();
@@ -587,34 +604,31 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) Cg[sigma(kt, q) * M + 8 * jt + p] = S.Cs[kt][jt][lane];
     __syncwarp();
-    double* Dm = &S.Cs[0][0][0];  // C is written back: reuse its smem for C~, row-major [R][M]
+    // C~ staged row-major (stride DS, conflict-free for the B operand below)
+    // over C's shared memory, which is written back already
+    constexpr int DS = M + 2;
+    double* Dm = &S.Cs[0][0][0];
 #pragma unroll
     for (int nt = 0; nt < IT; ++nt)
 #pragma unroll
       for (int J = 0; J < JK / 2; ++J) {
         const double2 v = make_double2(Dt[nt][2 * J], Dt[nt][2 * J + 1]);
         *reinterpret_cast<double2*>(Dg + (8 * nt + p) * M + 8 * J + 2 * q) = v;
-        *reinterpret_cast<double2*>(Dm + (8 * nt + p) * M + 8 * J + 2 * q) = v;
+        *reinterpret_cast<double2*>(Dm + (8 * nt + p) * DS + 8 * J + 2 * q) = v;
       }
-#pragma unroll
-    for (int nt = 0; nt < IT; ++nt) {
-      S.u.w[8 * nt + 2 * q][p] = Wt[nt][0];
-      S.u.w[8 * nt + 2 * q + 1][p] = Wt[nt][1];
-    }
     __syncwarp();
+    // x^T = x0^T + W^T C~ : M = c, N = j, K = i
 #pragma unroll
-    for (int ju = 0; ju < M / 32; ++ju) {
-      const int j = lane + 32 * ju;
-      double xs[KC];
-#pragma unroll
-      for (int c = 0; c < KC; ++c) xs[c] = has_x0 ? Xg[c * M + j] : 0.0;
-      for (int i = 0; i < r; ++i) {
-        const double d = Dm[i * M + j];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) xs[c] = fma(d, S.u.w[i][c], xs[c]);
+    for (int jt = 0; jt < JT; ++jt) {
+      double acc[2] = {0.0, 0.0};
+      if (has_x0) {
+        const double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * jt + 2 * q);
+        acc[0] = v.x;
+        acc[1] = v.y;
       }
 #pragma unroll
-      for (int c = 0; c < KC; ++c) Xg[c * M + j] = xs[c];
+      for (int kt = 0; kt < IK; ++kt) mma(acc, Wt[kt >> 1][kt & 1], Dm[sigma(kt, q) * DS + 8 * jt + p]);
+      *reinterpret_cast<double2*>(Xg + p * M + 8 * jt + 2 * q) = make_double2(acc[0], acc[1]);
     }
 #pragma unroll
     for (int mt = 0; mt < IT; ++mt)

@@ -1,0 +1,7 @@
+# bench line + ncu launch list of the same command + one full capture of the blocked kernel
+set -e
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_default.csv python bench.py > gpurun_out/ncu_launch_run.log 2>&1
+CMD="python bench.py --streams 8192 --steps 3 --warmup 3 --no-e2e --no-cpu"
+$CMD > gpurun_out/plain_small.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:blocked -s 3 -c 1 -o gpurun_out/prof_blocked_r1 $CMD > gpurun_out/ncu_full.log 2>&1
