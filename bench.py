@@ -35,7 +35,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_2106_11594_b200 import workloads  # noqa: E402
+from paper_2106_11594_b200 import sharding, workloads  # noqa: E402
 
 METRIC = "observation updates/sec (rows x streams, fp64) and % of fp64/HBM roofline"
 UNIT = "rows*streams/s"
@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4096)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return ap.parse_args()
 
 
@@ -261,15 +262,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    # one process per GPU; --dist-backend gloo lets a 1-GPU box exercise the
+    # multi-rank host logic (ranks share the device, no kernel waits on another)
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    device = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
     cfg = workloads.CONFIGS[args.config]
     B = args.streams or cfg.streams
-    if B % world:
-        raise SystemExit(f"{B} streams do not shard over {world} GPUs")
-    b0, b1 = rank * B // world, (rank + 1) * B // world
+    b0, b1 = sharding.shard_range(B, world, rank)
     S = b1 - b0
     tdtype = torch.float32 if args.dtype == "fp32" else torch.float64
     esize = 4 if args.dtype == "fp32" else 8
@@ -297,7 +302,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if args.dist_backend == "nccl":
+                dist.barrier(device_ids=[local_dev])
+            else:
+                dist.barrier()
 
     def step(ev=None):
         bs.reset()
@@ -311,7 +319,7 @@ def run_ours(args):
         step()
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -322,22 +330,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     barrier()
-    elapsed_ms = t0.elapsed_time(t1)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-    if world > 1:
-        t = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms, kern_ms = float(t[0]), float(t[1])
-        fl = torch.tensor([flops], dtype=torch.float64, device=device)
-        dist.all_reduce(fl)
-        flops_total = float(fl[0])
-        st = torch.tensor([int((status & 1).astype(bool).sum()), int((status & 2).astype(bool).sum())],
-                          dtype=torch.int64, device=device)
-        dist.all_reduce(st)
-        n_cap, n_nonfinite = int(st[0]), int(st[1])
-    else:
-        flops_total = flops
-        n_cap, n_nonfinite = int((status & 1).astype(bool).sum()), int((status & 2).astype(bool).sum())
+    # device time, max over ranks (sharding.py: no collective inside the timed region)
+    elapsed_ms = sharding.max_over_ranks(t0.elapsed_time(t1), device)
+    kern_ms = sharding.max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev), device)
+    flops_total = sharding.sum_over_ranks(flops, device)
+    n_cap = int(sharding.sum_over_ranks(int((status & 1).astype(bool).sum()), device))
+    n_nonfinite = int(sharding.sum_over_ranks(int((status & 2).astype(bool).sum()), device))
 
     total_rows = B * n
     value = total_rows * args.steps / (elapsed_ms * 1e-3)
@@ -374,12 +372,7 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, bs, rows, tg, stream, world, local, device, esize)
-        if world > 1:
-            t = torch.tensor([e2e.pop("_ms")], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t[0])
-        else:
-            ms = e2e.pop("_ms")
+        ms = sharding.max_over_ranks(e2e.pop("_ms"), device)
         e2e["value"] = B * n * e2e.pop("_steps") / (ms * 1e-3)
 
     cpu = None

@@ -193,7 +193,11 @@ def test_rank_capacity_grows_like_the_reference():
 # -- full-size configurations against the C oracle --------------------------------
 
 def ambiguous_rows(rho):
-    return (rho >= 0.25) & (rho <= 4.0)
+    """Rows whose oracle rank-test margin is within a factor 8 of the threshold:
+    a dependent row's rejection is pure rounding noise, whose size depends on
+    the summation order, so two correct fp64 implementations can land on
+    opposite sides of the threshold there (hard part 1)."""
+    return (rho >= 0.125) & (rho <= 8.0)
 
 
 def compare_to_oracle(rows, targets, res, r_cap, tol=TOL64, variant="general"):
@@ -300,3 +304,31 @@ def test_invariants_after_full_c5_ingest():
     bs.ingest(dev(rows[:, 64:128]), dev(tg[:, 64:128]), branch_log=br)
     assert int(br.sum()) == 0 and (bs.rank.cpu().numpy() == 16).all()
     assert np.isfinite(X).all()
+
+
+def test_c5_parity_at_scale_device_generated():
+    """4096 device-generated C5 streams at full length: every stream whose
+    oracle run has no near-threshold row (and no oracle rank runaway) must
+    match rank, branch sequence and x; the near-threshold rest is counted."""
+    from paper_2106_11594_b200 import workloads
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    rows_d, tg_d = workloads.device_batch("c5", 0, 4096, "cuda")
+    S, n, _ = rows_d.shape
+    bs = BatchedSolver(S, 64, k=8, r_cap=16)
+    br = torch.zeros((S, n), dtype=torch.uint8, device="cuda")
+    bs.ingest(rows_d, tg_d, branch_log=br)
+    torch.cuda.synchronize()
+    rows, tg = rows_d.cpu().numpy(), tg_d.cpu().numpy()
+    o = oracle.ingest(rows, tg, r_cap=16, nthreads=16)
+    amb = ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0)
+    ok = ~amb
+    st = bs.status.cpu().numpy()
+    assert (st[ok] == 0).all()
+    assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
+    assert np.array_equal(br.cpu().numpy()[ok], o["branch"][ok])
+    X = bs.solution.cpu().numpy()
+    XO = oracle.solution(o)
+    worst = max(relerr(X[b], XO[b]) for b in np.nonzero(ok)[0])
+    assert worst <= 1e-10
+    assert amb.mean() < 0.02, amb.mean()
