@@ -231,10 +231,12 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       for (int jt = 0; jt < JT; ++jt) X.acc[jt][0] = X.acc[jt][1] = 0.0;
     };
     // G = A C~^T (M = t, N = i, K = j; solver.py:286): K steps 2J, 2J + 1
-    auto front_g1 = [&](int s, int J, Front& F, FrontAcc& X) {
+    // (hi = false: rank <= 8, rows 8.. of C~ are zero and N tile 1 is skipped)
+    auto front_g1 = [&](int s, int J, Front& F, FrontAcc& X, bool hi = true) {
       const double2 v = reinterpret_cast<const double2*>(&S.At[s][0][lane][0])[J * 32];
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) {
+        if (nt > 0 && !hi) break;
         mma(F.g[nt], v.x, Dt[nt][2 * J]);
         mma(X.g2[nt], v.y, Dt[nt][2 * J + 1]);
       }
@@ -247,7 +249,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       }
     };
     // G C (M = t, N = j, K = i; solver.py:287): K step kt
-    auto front_g2 = [&](int kt, Front& F, FrontAcc& X) {
+    auto front_g2 = [&](int kt, Front& F, FrontAcc& X, bool hi = true) {
+      if (kt >= 2 && !hi) return;
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) mma(X.acc[jt], F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
     };
@@ -280,6 +283,25 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
       F.badm = __ballot_sync(FULL, q == 0 && valid && bad);
       F.tstar = stopm ? (__ffs(stopm) - 1) >> 2 : F.tv;
+      if (stopm) {
+        // keep what grow() needs of the stopping row: its coords gamma, its
+        // gain K = rej / |rej|^2 (solver.py:336; one rounding more than a
+        // division) and the row itself
+        if (p == F.tstar) {
+          const double rinv = 1.0 / rsq;
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+            *reinterpret_cast<double2*>(&S.u.ind.gam[8 * nt + 2 * q]) = make_double2(F.g[nt][0], F.g[nt][1]);
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double2 v = As[jt * 32];
+            *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
+                make_double2((v.x - X.acc[jt][0]) * rinv, (v.y - X.acc[jt][1]) * rinv);
+            *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) = v;
+          }
+        }
+        __syncwarp();
+      }
     };
     auto front = [&](int64_t tile, int s, int row_start, Front& F) {
       FrontAcc X;
@@ -462,40 +484,6 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 
     // independent row ts of front F (solver.py:305-318, _grow solver.py:368-397)
     auto grow = [&](const Front& F, int s, int ts) {
-      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
-      const double rs = __shfl_sync(FULL, F.rsq, 4 * ts);
-      if (p == ts) {
-#pragma unroll
-        for (int nt = 0; nt < IT; ++nt) {
-          S.u.ind.gam[8 * nt + 2 * q] = F.g[nt][0];
-          S.u.ind.gam[8 * nt + 2 * q + 1] = F.g[nt][1];
-        }
-      }
-      // the rejection of row ts on the current basis, recomputed (rare path;
-      // rows of C beyond the rank are zero, so only ceil(r/8) K pairs matter)
-      {
-        double acc[JT][2];
-#pragma unroll
-        for (int jt = 0; jt < JT; ++jt) acc[jt][0] = acc[jt][1] = 0.0;
-#pragma unroll
-        for (int kt = 0; kt < IK; ++kt) {
-          if (kt >= 2 && r <= 8) break;
-#pragma unroll
-          for (int jt = 0; jt < JT; ++jt) mma(acc[jt], F.g[kt >> 1][kt & 1], S.Cs[kt][jt][lane]);
-        }
-        // K = rej / |rej|^2 (solver.py:336); one rounding more than a division
-        const double rinv = 1.0 / rs;
-        if (p == ts) {
-#pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
-            const double2 v = As[jt * 32];
-            *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
-                make_double2((v.x - acc[jt][0]) * rinv, (v.y - acc[jt][1]) * rinv);
-            *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) = v;
-          }
-        }
-      }
-      __syncwarp();
       // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
       const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
       const double wnew = __shfl_sync(FULL, dv, 4 * p + (ts >> 1));
