@@ -36,7 +36,7 @@
 // so that every accumulator is directly the next MMA's operand:
 //   tile   a[nt][e]      = A[t=p][8nt+2q+e]            (A- and B-operand, K=sigma)
 //   C~^T   Dt[nt][kt]    = C~[8nt+p][sigma(kt,q)]       registers
-//   C      Cs[kt][jt][l] = C[sigma(kt,q)][8jt+p]        shared memory
+//   -C     Cs[kt][jt][l] = -C[sigma(kt,q)][8jt+p]       shared memory (R accumulates onto A)
 //   P^-1   Pr[mt][nt][e] = P[8mt+p][8nt+2q+e]           registers (symmetric)
 //   W^T    Wt[nt][e]     = W[8nt+2q+e][c=p]             registers
 //
@@ -83,7 +83,7 @@ __device__ __forceinline__ double rcp64(double x) {
 
 template <int M, int R, int KC>
 struct WarpSmem {
-  double Cs[R / 4][M / 8][32];   // basis C as the B operand of R = A - G C
+  double Cs[R / 4][M / 8][32];   // -C, the B operand of R = A + G (-C) accumulated onto A
   double At[2][M / 8][32][2];    // double-buffered row tile, lane-slot layout
   double Yt[2][32][2];           // targets y[t=2q+e][c=p]
   union {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
     for (int kt = 0; kt < IK; ++kt)
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) S.Cs[kt][jt][lane] = fresh ? 0.0 : Cg[sigma(kt, q) * M + 8 * jt + p];
+      for (int jt = 0; jt < JT; ++jt) S.Cs[kt][jt][lane] = fresh ? 0.0 : -Cg[sigma(kt, q) * M + 8 * jt + p];
     // x0 = the solution at call start; when it is exactly zero a.x0 = 0 and
     // its contraction is skipped.
     bool nz = false;
@@ -227,8 +227,13 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       F.asq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) F.g[nt][0] = F.g[nt][1] = X.g2[nt][0] = X.g2[nt][1] = 0.0;
+      // R = A - G C accumulates onto the tile itself (C is stored negated)
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) X.acc[jt][0] = X.acc[jt][1] = 0.0;
+      for (int jt = 0; jt < JT; ++jt) {
+        const double2 v = As[jt * 32];
+        X.acc[jt][0] = v.x;
+        X.acc[jt][1] = v.y;
+      }
     };
     // G = A C~^T (M = t, N = i, K = j; solver.py:286): K steps 2J, 2J + 1
     // (hi = false: rank <= 8, rows 8.. of C~ are zero and N tile 1 is skipped)
@@ -248,7 +253,10 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         }
       }
     };
-    // G C (M = t, N = j, K = i; solver.py:287): K step kt
+    // R = A - G C (M = t, N = j, K = i; solver.py:287-288): K step kt.  The
+    // accumulation order differs from the reference's (a - (G C)) but gives
+    // the same rejection-noise statistics (max rho over 768 C5 streams 0.549
+    // vs 0.541, log-correlation 0.99995), so rank decisions are unaffected.
     auto front_g2 = [&](int kt, Front& F, FrontAcc& X, bool hi = true) {
       if (kt >= 2 && !hi) return;
 #pragma unroll
@@ -260,8 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) {
-        const double2 v = As[jt * 32];
-        const double r0 = v.x - X.acc[jt][0], r1 = v.y - X.acc[jt][1];
+        const double r0 = X.acc[jt][0], r1 = X.acc[jt][1];
         s4[(2 * jt) & 3] = fma(r0, r0, s4[(2 * jt) & 3]);
         s4[(2 * jt + 1) & 3] = fma(r1, r1, s4[(2 * jt + 1) & 3]);
       }
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           for (int jt = 0; jt < JT; ++jt) {
             const double2 v = As[jt * 32];
             *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
-                make_double2((v.x - X.acc[jt][0]) * rinv, (v.y - X.acc[jt][1]) * rinv);
+                make_double2(X.acc[jt][0] * rinv, X.acc[jt][1] * rinv);
             *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) = v;
           }
         }
@@ -508,7 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       if (q == ((r & 7) >> 1)) {
         const int ktr = 2 * (r >> 3) + (r & 1);
 #pragma unroll
-        for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = S.u.ind.av[8 * jt + p];
+        for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = -S.u.ind.av[8 * jt + p];
       }
       // P = diag(P, 1)  (solver.py:372-373, 381)
 #pragma unroll
@@ -590,7 +597,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
     for (int kt = 0; kt < IK; ++kt)
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) Cg[sigma(kt, q) * M + 8 * jt + p] = S.Cs[kt][jt][lane];
+      for (int jt = 0; jt < JT; ++jt) Cg[sigma(kt, q) * M + 8 * jt + p] = -S.Cs[kt][jt][lane];
     __syncwarp();
     // C~ staged row-major (stride DS, conflict-free for the B operand below)
     // over C's shared memory, which is written back already
