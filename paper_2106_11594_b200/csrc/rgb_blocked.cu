@@ -42,44 +42,10 @@
 //
 // Specialised for the batched configuration m = 64, r_cap = 16, k = 8 (fp64,
 // general variant); every other shape runs on rgb_generic.cu.
-#include "rgb_common.cuh"
+#include "rgb_mma.cuh"
 
 namespace rgb {
 namespace blk {
-
-constexpr unsigned FULL = 0xffffffffu;
-constexpr int TT = 8;  // rows per tile
-
-__device__ __forceinline__ void mma(double (&d)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d[0]), "+d"(d[1])
-      : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-__device__ __forceinline__ int sigma(int kt, int q) { return 8 * (kt >> 1) + 2 * q + (kt & 1); }
-
-// 1/x to within an ulp without branches: MUFU.RCP64H seed (rcp.approx.ftz.f64)
-// and two Newton steps.  Only used for LDL^T pivots of I + G P G^T (>= 1).
-__device__ __forceinline__ double rcp64(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 template <int M, int R, int KC>
 struct WarpSmem {

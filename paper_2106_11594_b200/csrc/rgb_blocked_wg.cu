@@ -1,0 +1,535 @@
+// rgb_blocked_wg.cu -- batched rank-Greville update for wider streams: one
+// warp GROUP per stream (sm_100a, fp64 tensor cores).
+//
+// Same algorithm as rgb_blocked.cu (8-row tiles, tensor-core projections,
+// LDL^T-factored Sherman-Morrison, x = x0 + C~^T W; see its header), for
+// shapes whose factors do not fit one warp: the 32*WG columns of a stream are
+// split over WG warps (warp w owns columns [32w, 32w+32)), and the r_cap rows
+// of P^-1 and W over the same warps by 8-row tiles.  Contractions over the
+// columns (G = A C~^T, |a|^2, |rej|^2, a.x0) are reduced across the group
+// through shared memory in a fixed order (deterministic); the 8x8 LDL^T is
+// computed redundantly by every warp.  Built for config 3 of BASELINE.json
+// (m = 128, r <= 32, k = 1): WG = 4, r_cap = 32.
+//
+// Per warp w, lane = 4p + q (fragment layouts of mma.m8n8k4.f64):
+//   tile   As[nt][l]   = A[t=p][32w + 8nt + 2q + e]
+//   C~^T   Dt[nt][kt]  = C~[8nt + p][32w + sigma(kt,q)]        registers
+//   -C     Cs[kt][jt][l] = -C[sigma(kt,q)][32w + 8jt + p]     shared memory
+//   P^-1   Pr[nt][e]   = P[8w + p][8nt + 2q + e]   (row block w, symmetric)
+//   W^T    Wt[e]       = W[8w + 2q + e][c = p]     (row block w)
+#include "rgb_mma.cuh"
+
+namespace rgb {
+namespace blk {
+
+template <int R, int WG>
+struct GroupSmem {
+  static constexpr int M = 32 * WG, IT = R / 8, IK = R / 4;
+  double Cs[WG][IK][4][32];          // -C, per warp column slice
+  double At[WG][2][4][32][2];        // row tiles, per warp column slice, 2 stages
+  double Yt[WG][2][32][2];           // targets y[t=2q+e][c=p], per warp copy
+  double Gp[WG][IT][32][2];          // partial G of each warp
+  double red[3][WG][32][2];          // asq / rsq / dyx partials
+  double Sp[WG][32][2];              // partial S (and G W)
+  double Yb[IT][32][2];              // Y^T tiles exchanged for the P update
+  double gam[R];                     // independent row: coords
+  double kv[M];                      //                  gain K
+  double av[M];                      //                  the row
+};
+
+template <int R, int WG>
+__global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
+    rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
+    const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
+    double* __restrict__ clog) {
+  constexpr int M = 32 * WG, IT = R / 8, IK = R / 4, KC = 8;
+  static_assert(R % 8 == 0 && R <= 32 && IT <= WG, "shape");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GroupSmem<R, WG>& S = *reinterpret_cast<GroupSmem<R, WG>*>(smem_raw);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int p = lane >> 2, q = lane & 3;
+  const int k = cfg.k;
+  const int j0 = 32 * w;
+
+  for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
+    int status = st.status[b];
+    if (status) continue;  // uniform across the block
+    int r = st.rank[b];
+    const int64_t nobs0 = st.nobs[b];
+    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
+    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
+    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
+    double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
+    const double* Rb = rows + b * rstride;
+    const double* Yb = tgts + b * tstride;
+
+    // ---- state (rank 0 is all zeros by the state contract) ------------------------
+    const bool fresh = (r == 0);
+    double Dt[IT][8];
+    double Pr[IT][2];
+    double Wt[2] = {0.0, 0.0};
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt) {
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const double2 v = fresh ? make_double2(0.0, 0.0)
+                                : *reinterpret_cast<const double2*>(Dg + (8 * nt + p) * M + j0 + 8 * J + 2 * q);
+        Dt[nt][2 * J] = v.x;
+        Dt[nt][2 * J + 1] = v.y;
+      }
+      const double2 v = (fresh || w >= IT) ? make_double2(0.0, 0.0)
+                                           : *reinterpret_cast<const double2*>(Pg + (8 * w + p) * R + 8 * nt + 2 * q);
+      Pr[nt][0] = v.x;
+      Pr[nt][1] = v.y;
+    }
+#pragma unroll
+    for (int kt = 0; kt < IK; ++kt)
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) S.Cs[w][kt][jt][lane] = fresh ? 0.0 : -Cg[sigma(kt, q) * M + j0 + 8 * jt + p];
+    bool nz = false;
+    if (!fresh && p < k) {
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const double2 v = *reinterpret_cast<const double2*>(Xg + p * M + j0 + 8 * J + 2 * q);
+        nz |= (v.x != 0.0) || (v.y != 0.0);
+      }
+    }
+    const bool has_x0 = __syncthreads_or(nz) != 0;
+
+    const int64_t ntiles = (T + TT - 1) / TT;
+    auto prefetch = [&](int64_t tile, int s) {
+      if (tile < ntiles) {
+        const int64_t t0 = tile * TT;
+        const int64_t t = t0 + p;
+        const bool ok = t < T;
+        const double* src = ok ? Rb + t * M + j0 : Rb;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) cp_async16(&S.At[w][s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t ty = t0 + 2 * q + e;
+          const bool oky = ty < T && p < k;
+          cp_async8(&S.Yt[w][s][lane][e], oky ? Yb + ty * k + p : Yb, oky ? 8 : 0);
+        }
+      }
+      cp_commit();
+    };
+
+    struct Front {
+      double g[IT][2];   // G[t=p][8nt+2q+e] (full, identical in every warp)
+      double acc[4][2];  // rejection of the own columns: A - G C
+      double rsq, asq;   // |rej_t|^2, |a_t|^2 for t = p
+      double dyx[2];     // y - a.x0 for (c = p, t = 2q+e)
+      unsigned badm;
+      int tstar, tv;
+      int64_t t0;
+    };
+
+    // projection of one tile and the rank test (solver.py:286-296)
+    auto front = [&](int64_t tile, int s, int row_start, Front& F) {
+      const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
+      F.t0 = tile * TT;
+      F.tv = (int)((T - F.t0) < TT ? (T - F.t0) : TT);
+      const double2 yy = *reinterpret_cast<const double2*>(&S.Yt[w][s][lane][0]);
+      const int nti = (r + 7) >> 3;  // N tiles of G that can be nonzero
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      double g[IT][2], g2[IT][2];
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = g2[nt][0] = g2[nt][1] = 0.0;
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const double2 v = As[J * 32];
+        s4[(2 * J) & 3] = fma(v.x, v.x, s4[(2 * J) & 3]);
+        s4[(2 * J + 1) & 3] = fma(v.y, v.y, s4[(2 * J + 1) & 3]);
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          if (nt < nti) {
+            mma(g[nt], v.x, Dt[nt][2 * J]);
+            mma(g2[nt], v.y, Dt[nt][2 * J + 1]);
+          }
+        }
+      }
+      double asq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      asq += __shfl_xor_sync(FULL, asq, 1);
+      asq += __shfl_xor_sync(FULL, asq, 2);
+      // a.x0 of the own columns (M = c, N = t, K = j) when x0 != 0
+      double y0[2] = {0.0, 0.0};
+      if (has_x0) {
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          double2 xv = make_double2(0.0, 0.0);
+          if (p < k) xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + j0 + 8 * J + 2 * q));
+          const double2 v = As[J * 32];
+          mma(y0, xv.x, v.x);
+          mma(y0, xv.y, v.y);
+        }
+      }
+      // cross-warp sums: G partials, |a|^2, a.x0
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt)
+        *reinterpret_cast<double2*>(&S.Gp[w][nt][lane][0]) = make_double2(g[nt][0] + g2[nt][0], g[nt][1] + g2[nt][1]);
+      *reinterpret_cast<double2*>(&S.red[0][w][lane][0]) = make_double2(asq, 0.0);
+      *reinterpret_cast<double2*>(&S.red[2][w][lane][0]) = make_double2(y0[0], y0[1]);
+      __syncthreads();
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        double2 sum = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < WG; ++u) {
+          const double2 v = *reinterpret_cast<const double2*>(&S.Gp[u][nt][lane][0]);
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+        F.g[nt][0] = sum.x;
+        F.g[nt][1] = sum.y;
+      }
+      asq = 0.0;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int u = 0; u < WG; ++u) {
+        asq += S.red[0][u][lane][0];
+        a0 += S.red[2][u][lane][0];
+        a1 += S.red[2][u][lane][1];
+      }
+      F.asq = asq;
+      F.dyx[0] = yy.x - a0;
+      F.dyx[1] = yy.y - a1;
+      // R = A - G C on the own columns (C stored negated, accumulated onto A)
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+        const double2 v = As[jt * 32];
+        F.acc[jt][0] = v.x;
+        F.acc[jt][1] = v.y;
+      }
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) {
+        if (8 * (kt >> 1) < r) {  // rows of C beyond the rank are zero
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt) mma(F.acc[jt], F.g[kt >> 1][kt & 1], S.Cs[w][kt][jt][lane]);
+        }
+      }
+      double t4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+        t4[(2 * jt) & 3] = fma(F.acc[jt][0], F.acc[jt][0], t4[(2 * jt) & 3]);
+        t4[(2 * jt + 1) & 3] = fma(F.acc[jt][1], F.acc[jt][1], t4[(2 * jt + 1) & 3]);
+      }
+      double rsq = (t4[0] + t4[1]) + (t4[2] + t4[3]);
+      rsq += __shfl_xor_sync(FULL, rsq, 1);
+      rsq += __shfl_xor_sync(FULL, rsq, 2);
+      S.red[1][w][lane][0] = rsq;
+      __syncthreads();
+      rsq = 0.0;
+#pragma unroll
+      for (int u = 0; u < WG; ++u) rsq += S.red[1][u][lane][0];
+      F.rsq = rsq;
+      const unsigned yb0 = __ballot_sync(FULL, !isfinite(F.dyx[0]));
+      const unsigned yb1 = __ballot_sync(FULL, !isfinite(F.dyx[1]));
+      const bool ybad = (((p & 1) ? yb1 : yb0) & (0x11111111u << (p >> 1))) != 0u;
+      const bool valid = p >= row_start && p < F.tv;
+      const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
+      const bool bad = !isfinite(asq) || ybad;
+      const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
+      F.badm = __ballot_sync(FULL, q == 0 && valid && bad);
+      F.tstar = stopm ? (__ffs(stopm) - 1) >> 2 : F.tv;
+    };
+
+    // blocked Sherman-Morrison over the dependent rows [rs, te) (solver.py:297-304)
+    auto scan = [&](const Front& F, int rs, int te) {
+      const bool inb = p >= rs && p < te;
+      double gm[IT][2];
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        gm[nt][0] = inb ? F.g[nt][0] : 0.0;
+        gm[nt][1] = inb ? F.g[nt][1] : 0.0;
+      }
+      const bool own = w < IT;  // warps beyond the P / W row blocks only help the front
+      // (G W)^T over the own row block of W, and U^T = G P[:, own block]
+      double gw[2] = {0.0, 0.0}, ut[2] = {0.0, 0.0};
+      if (own) {
+        mma(gw, Wt[0], gm[w][0]);
+        mma(gw, Wt[1], gm[w][1]);
+#pragma unroll
+        for (int kt = 0; kt < IK; ++kt) mma(ut, gm[kt >> 1][kt & 1], Pr[kt >> 1][kt & 1]);
+      }
+      // S partial = U^T[:, own] G[:, own]^T
+      double sp[2] = {0.0, 0.0};
+      if (own) {
+        mma(sp, ut[0], gm[w][0]);
+        mma(sp, ut[1], gm[w][1]);
+      }
+      *reinterpret_cast<double2*>(&S.Sp[w][lane][0]) = make_double2(sp[0], sp[1]);
+      *reinterpret_cast<double2*>(&S.red[2][w][lane][0]) = make_double2(gw[0], gw[1]);
+      __syncthreads();
+      double mi[2] = {0.0, 0.0}, gws[2] = {0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < WG; ++u) {
+        mi[0] += S.Sp[u][lane][0];
+        mi[1] += S.Sp[u][lane][1];
+        gws[0] += S.red[2][u][lane][0];
+        gws[1] += S.red[2][u][lane][1];
+      }
+      double dy[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = 2 * q + e;
+        dy[e] = (t >= rs && t < te) ? F.dyx[e] - gws[e] : 0.0;
+      }
+      if (p == 2 * q) mi[0] += 1.0;
+      if (p == 2 * q + 1) mi[1] += 1.0;
+      // M = L diag(d) L^T, E = L^-1 (every warp, identical)
+      double ev[2] = {p == 2 * q ? 1.0 : 0.0, p == 2 * q + 1 ? 1.0 : 0.0};
+#pragma unroll
+      for (int kk = 0; kk < TT - 1; ++kk) {
+        const double v = (kk & 1) ? mi[1] : mi[0];
+        const double piv = __shfl_sync(FULL, v, 4 * kk + (kk >> 1));
+        const double mps = __shfl_sync(FULL, v, 4 * p + (kk >> 1));
+        const double m0 = __shfl_sync(FULL, mi[0], 4 * kk + q);
+        const double m1 = __shfl_sync(FULL, mi[1], 4 * kk + q);
+        const double e0 = __shfl_sync(FULL, ev[0], 4 * kk + q);
+        const double e1 = __shfl_sync(FULL, ev[1], 4 * kk + q);
+        const double f = (p > kk) ? mps * rcp64(piv) : 0.0;
+        mi[0] = fma(-f, m0, mi[0]);
+        mi[1] = fma(-f, m1, mi[1]);
+        ev[0] = fma(-f, e0, ev[0]);
+        ev[1] = fma(-f, e1, ev[1]);
+      }
+      const double dsel = (p & 1) ? mi[1] : mi[0];
+      const double rd = rcp64(__shfl_sync(FULL, dsel, 4 * p + (p >> 1)));
+      const double rd0 = __shfl_sync(FULL, rd, 8 * q);
+      const double rd1 = __shfl_sync(FULL, rd, 8 * q + 4);
+      // U = (U^T)^T on the own block, Y^T = U E^T (rows of the own block)
+      double yt[2] = {0.0, 0.0};
+      if (own) {
+        double u[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int src = 4 * (2 * q + e) + (p >> 1);
+          const double v0 = __shfl_sync(FULL, ut[0], src);
+          const double v1 = __shfl_sync(FULL, ut[1], src);
+          u[e] = (p & 1) ? v1 : v0;
+        }
+        mma(yt, u[0], ev[0]);
+        mma(yt, u[1], ev[1]);
+        *reinterpret_cast<double2*>(&S.Yb[w][lane][0]) = make_double2(yt[0], yt[1]);
+      }
+      __syncthreads();
+      if (own) {
+        // E dy0 (every RHS), then P[own rows] -= Y^T D^-1 Y and W[own] += ...
+        double dh[2] = {0.0, 0.0};
+        mma(dh, dy[0], ev[0]);
+        mma(dh, dy[1], ev[1]);
+        const double d0 = dh[0] * rd0, d1 = dh[1] * rd1;
+        const double s0 = -yt[0] * rd0, s1 = -yt[1] * rd1;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          const double2 yb = *reinterpret_cast<const double2*>(&S.Yb[nt][lane][0]);
+          mma(Pr[nt], s0, yb.x);
+          mma(Pr[nt], s1, yb.y);
+        }
+        mma(Wt, d0, yt[0]);
+        mma(Wt, d1, yt[1]);
+      }
+      if (inb && w == 0) {
+        const int64_t row = b * T + F.t0 + p;
+        if (blog && q == 0) blog[row] = 0;
+        if (clog) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+            *reinterpret_cast<double2*>(clog + row * R + 8 * nt + 2 * q) = make_double2(F.g[nt][0], F.g[nt][1]);
+        }
+      }
+    };
+
+    // independent row ts (solver.py:305-318, _grow solver.py:368-397)
+    auto grow = [&](const Front& F, int s, int ts) {
+      if (p == ts) {
+        const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
+        const double rinv = 1.0 / F.rsq;  // K = rej / |rej|^2, one rounding more than a division
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+          *reinterpret_cast<double2*>(&S.kv[j0 + 8 * jt + 2 * q]) =
+              make_double2(F.acc[jt][0] * rinv, F.acc[jt][1] * rinv);
+          *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) = As[jt * 32];
+        }
+        if (w == 0) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+            *reinterpret_cast<double2*>(&S.gam[8 * nt + 2 * q]) = make_double2(F.g[nt][0], F.g[nt][1]);
+        }
+      }
+      __syncthreads();
+      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
+      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
+      const double wnew = __shfl_sync(FULL, dv, 4 * p + (ts >> 1));
+      if (w == (r >> 3)) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (8 * w + 2 * q + e == r) Wt[e] = wnew;
+      }
+      // C~[:r] -= gamma K^T, C~[r] = K on the own columns (solver.py:377-380)
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        const int i = 8 * nt + p;
+        const double gi = S.gam[i];
+#pragma unroll
+        for (int J = 0; J < 4; ++J) {
+          const double2 kv = *reinterpret_cast<const double2*>(&S.kv[j0 + 8 * J + 2 * q]);
+          Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
+          Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
+        }
+      }
+      // C[r] = a
+      if (q == ((r & 7) >> 1)) {
+        const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) S.Cs[w][ktr][jt][lane] = -S.av[j0 + 8 * jt + p];
+      }
+      // P = diag(P, 1)
+      if (w < IT) {
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = 8 * w + p, i2 = 8 * nt + 2 * q + e;
+            if (i == r || i2 == r) Pr[nt][e] = (i == i2) ? 1.0 : 0.0;
+          }
+      }
+      const int64_t row = b * T + F.t0 + ts;
+      if (w == 0) {
+        if (blog && lane == 0) blog[row] = 1;
+        if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      r += 1;
+    };
+
+    bool stopped = false;
+    int64_t consumed = 0;
+    Front F;
+    if (ntiles > 0) {
+      prefetch(0, 0);
+      prefetch(1, 1);
+      cp_wait<1>();
+      __syncwarp();
+    }
+    for (int64_t tile = 0; tile < ntiles; ++tile) {
+      const int s = (int)(tile & 1);
+      int row_start = 0;
+      front(tile, s, 0, F);
+      while (true) {
+        if (F.tstar > row_start) scan(F, row_start, F.tstar);
+        if (F.tstar >= F.tv) break;
+        if ((F.badm >> (4 * F.tstar)) & 1u) {
+          status |= RGB_ST_NONFINITE;
+          stopped = true;
+          break;
+        }
+        if (r >= R) {
+          status |= RGB_ST_RANK_CAP;
+          stopped = true;
+          break;
+        }
+        grow(F, s, F.tstar);
+        row_start = F.tstar + 1;
+        if (row_start >= F.tv) break;
+        front(tile, s, row_start, F);
+      }
+      if (stopped) {
+        consumed = F.t0 + F.tstar;
+        break;
+      }
+      consumed = F.t0 + F.tv;
+      __syncthreads();  // every warp is done with stage s before it is refilled
+      prefetch(tile + 2, s);
+      cp_wait<1>();
+      __syncwarp();
+    }
+    cp_wait<0>();
+    __syncthreads();
+
+    // ---- write back; x = x0 + C~^T W ------------------------------------------------
+#pragma unroll
+    for (int kt = 0; kt < IK; ++kt)
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) Cg[sigma(kt, q) * M + j0 + 8 * jt + p] = -S.Cs[w][kt][jt][lane];
+    // W of every row block, for the x contraction of the own columns
+    if (w < IT) *reinterpret_cast<double2*>(&S.Yb[w][lane][0]) = make_double2(Wt[0], Wt[1]);
+    __syncwarp();
+    // C~ of the own columns, staged row-major over the own Cs slice
+    double* Dm = &S.Cs[w][0][0][0];
+    constexpr int DS = 32;
+    static_assert(sizeof(S.Cs[0]) >= sizeof(double) * R * DS, "staging");
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {
+        const double2 v = make_double2(Dt[nt][2 * J], Dt[nt][2 * J + 1]);
+        *reinterpret_cast<double2*>(Dg + (8 * nt + p) * M + j0 + 8 * J + 2 * q) = v;
+        *reinterpret_cast<double2*>(Dm + (8 * nt + p) * DS + 8 * J + 2 * q) = v;
+      }
+    __syncthreads();
+    // x^T = x0^T + W^T C~ : M = c, N = j (own), K = i
+#pragma unroll
+    for (int jt = 0; jt < 4; ++jt) {
+      double acc[2] = {0.0, 0.0};
+      if (has_x0 && p < k) {
+        const double2 v = *reinterpret_cast<const double2*>(Xg + p * M + j0 + 8 * jt + 2 * q);
+        acc[0] = v.x;
+        acc[1] = v.y;
+      }
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) {
+        const double a = S.Yb[kt >> 1][lane][kt & 1];
+        mma(acc, a, Dm[sigma(kt, q) * DS + 8 * jt + p]);
+      }
+      if (p < k) *reinterpret_cast<double2*>(Xg + p * M + j0 + 8 * jt + 2 * q) = make_double2(acc[0], acc[1]);
+    }
+    if (w < IT) {
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt)
+        *reinterpret_cast<double2*>(Pg + (8 * w + p) * R + 8 * nt + 2 * q) = make_double2(Pr[nt][0], Pr[nt][1]);
+    }
+    if (threadIdx.x == 0) {
+      st.rank[b] = r;
+      st.nobs[b] = nobs0 + consumed;
+      st.status[b] = status;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace blk
+
+namespace {
+constexpr int WGM = 128, WGR = 32, WGW = 4;
+}  // namespace
+
+bool blocked_wg_supports(const rgb_config& cfg) {
+  return cfg.dtype == RGB_F64 && cfg.variant == RGB_GENERAL && cfg.m == WGM && cfg.r_cap == WGR &&
+         cfg.k >= 1 && cfg.k <= 8;
+}
+
+int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                      cudaStream_t stream, int num_sms) {
+  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
+  auto kern = blk::blocked_wg_kernel<WGR, WGW>;
+  const size_t smem = sizeof(blk::GroupSmem<WGR, WGW>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WGW * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)num_sms * per_sm;
+  if (grid > cfg.num_streams) grid = cfg.num_streams;
+  kern<<<(unsigned)grid, WGW * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
+                                                   (const double*)targets, tg_stride, T, logs.branch,
+                                                   (double*)logs.coords);
+  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+}  // namespace rgb
