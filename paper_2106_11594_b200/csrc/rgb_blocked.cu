@@ -456,10 +456,9 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     };
 
     // independent row ts of front F (solver.py:305-318, _grow solver.py:368-397)
-    auto grow = [&](const Front& F, int s, int ts) {
-      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
-      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
-      const double wnew = __shfl_sync(FULL, dv, 4 * p + (ts >> 1));
+    // grow_core: the independent-row update from the scratch rows written by
+    // front_end() or project_row(); wnew = y - a.x0 of the row for RHS c = p
+    auto grow_core = [&](double wnew, int64_t t0, int ts) {
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt)
 #pragma unroll
@@ -493,25 +492,124 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
             const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
             if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
           }
-      const int64_t row = b * T + F.t0 + ts;
+      const int64_t row = b * T + t0 + ts;
       if (blog && lane == 0) blog[row] = 1;
       if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
       __syncwarp();
       r += 1;
     };
+    auto grow = [&](const Front& F, int ts) {
+      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
+      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
+      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), F.t0, ts);
+    };
+
+    // Single-row projection of row ts of stage s on the current basis, on the
+    // CUDA cores (solver.py:286-291): used while a fresh stream's leading rows
+    // are independent, where re-projecting a whole 8-row tile after every
+    // basis growth would cost 64 MMAs per row.  Leaves gamma, K = rej/|rej|^2
+    // and the row in the scratch rows for grow_core(); returns |rej|^2, |a|^2.
+    auto project_row = [&](int s, int ts, double& rsq_o, double& asq_o) {
+      const double2* Ar = reinterpret_cast<const double2*>(&S.At[s][0][4 * ts + q][0]);
+      double gp[IT], a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) gp[nt] = 0.0;
+#pragma unroll
+      for (int J = 0; J < JK / 2; ++J) {  // my columns sigma(kt, q) = 8J + 2q + e
+        const double2 v = Ar[J * 32];
+        a4[(2 * J) & 3] = fma(v.x, v.x, a4[(2 * J) & 3]);
+        a4[(2 * J + 1) & 3] = fma(v.y, v.y, a4[(2 * J + 1) & 3]);
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) gp[nt] = fma(Dt[nt][2 * J], v.x, fma(Dt[nt][2 * J + 1], v.y, gp[nt]));
+      }
+      double asq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      asq += __shfl_xor_sync(FULL, asq, 1);
+      asq += __shfl_xor_sync(FULL, asq, 2);
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        gp[nt] += __shfl_xor_sync(FULL, gp[nt], 1);
+        gp[nt] += __shfl_xor_sync(FULL, gp[nt], 2);
+      }
+      // gamma[8nt + p] = gp[nt] in quad p; rej_j = a_j - sum_i gamma_i C_ij
+      // for my Cs columns j = 8jt + p over my rows i = sigma(kt, q)
+      double rp[JT];
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) rp[jt] = 0.0;
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) {
+        const double gi = __shfl_sync(FULL, gp[kt >> 1], 4 * (2 * q + (kt & 1)));
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) rp[jt] = fma(gi, S.Cs[kt][jt][lane], rp[jt]);  // Cs = -C
+      }
+      double r4[4] = {0.0, 0.0, 0.0, 0.0};
+      double rej[JT];
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) {
+        rp[jt] += __shfl_xor_sync(FULL, rp[jt], 1);
+        rp[jt] += __shfl_xor_sync(FULL, rp[jt], 2);
+        rej[jt] = S.At[s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
+        r4[jt & 3] = fma(rej[jt], rej[jt], r4[jt & 3]);
+      }
+      double rsq = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+      rsq += __shfl_xor_sync(FULL, rsq, 4);
+      rsq += __shfl_xor_sync(FULL, rsq, 8);
+      rsq += __shfl_xor_sync(FULL, rsq, 16);
+      if (q == 0) {
+        const double rinv = 1.0 / rsq;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) S.u.ind.gam[8 * nt + p] = gp[nt];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+          S.u.ind.kv[8 * jt + p] = rej[jt] * rinv;
+          S.u.ind.av[8 * jt + p] = S.At[s][jt][4 * ts + (p >> 1)][p & 1];
+        }
+      }
+      __syncwarp();
+      rsq_o = rsq;
+      asq_o = asq;
+    };
 
     bool stopped = false;
     Front F;
+    int64_t tile = 0;
+    int first_row = 0;  // rows of the first blocked tile already consumed in row mode
     if (ntiles > 0) {
       prefetch(0, 0);
       prefetch(1, 1);
       cp_wait<1>();
-      front(0, 0, 0, F);
-      front_x0(0, F);
+      // row mode: a fresh stream's leading independent rows, one at a time
+      if (fresh) {
+        while (tile < ntiles) {
+          const int s = (int)(tile & 1);
+          const int64_t t0 = tile * TT;
+          const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
+          int ts = 0;
+          for (; ts < tv; ++ts) {
+            double rsq, asq;
+            project_row(s, ts, rsq, asq);
+            const double yv = S.Yt[s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p]
+            const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
+            if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
+            grow_core(yv, t0, ts);
+          }
+          if (ts < tv) {
+            first_row = ts;
+            break;
+          }
+          consumed = t0 + tv;
+          ++tile;
+          prefetch(tile + 1, s);
+          cp_wait<1>();
+        }
+      }
+      if (tile < ntiles) {
+        front(tile, (int)(tile & 1), first_row, F);
+        front_x0((int)(tile & 1), F);
+      }
     }
-    for (int64_t tile = 0; tile < ntiles; ++tile) {
+    for (; tile < ntiles; ++tile) {
       const int s = (int)(tile & 1);
-      if (F.tstar >= F.tv) {
+      if (F.tstar >= F.tv && first_row == 0) {
         // every row of the tile is dependent: scan(i) overlaps front(i+1)
         prefetch(tile + 2, s);
         cp_wait<1>();
@@ -523,7 +621,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         F = N;
         continue;
       }
-      int row_start = 0;
+      int row_start = first_row;
+      first_row = 0;
       while (true) {
         if (F.tstar > row_start) {
           scan(F, row_start, F.tstar);
@@ -540,7 +639,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           stopped = true;
           break;
         }
-        grow(F, s, F.tstar);
+        grow(F, F.tstar);
         row_start = F.tstar + 1;
         if (row_start >= F.tv) break;
         front(tile, s, row_start, F);   // re-project the rest of the tile on the new basis
