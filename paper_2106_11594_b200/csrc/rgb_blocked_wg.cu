@@ -341,27 +341,8 @@ __global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
       }
     };
 
-    // independent row ts (solver.py:305-318, _grow solver.py:368-397)
-    auto grow = [&](const Front& F, int s, int ts) {
-      if (p == ts) {
-        const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
-        const double rinv = 1.0 / F.rsq;  // K = rej / |rej|^2, one rounding more than a division
-#pragma unroll
-        for (int jt = 0; jt < 4; ++jt) {
-          *reinterpret_cast<double2*>(&S.kv[j0 + 8 * jt + 2 * q]) =
-              make_double2(F.acc[jt][0] * rinv, F.acc[jt][1] * rinv);
-          *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) = As[jt * 32];
-        }
-        if (w == 0) {
-#pragma unroll
-          for (int nt = 0; nt < IT; ++nt)
-            *reinterpret_cast<double2*>(&S.gam[8 * nt + 2 * q]) = make_double2(F.g[nt][0], F.g[nt][1]);
-        }
-      }
-      __syncthreads();
-      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
-      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
-      const double wnew = __shfl_sync(FULL, dv, 4 * p + (ts >> 1));
+    // the update itself, from the scratch rows (gam, kv, av)
+    auto grow_core = [&](double wnew, int64_t t0, int ts) {
       if (w == (r >> 3)) {
 #pragma unroll
         for (int e = 0; e < 2; ++e)
@@ -395,7 +376,7 @@ __global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
             if (i == r || i2 == r) Pr[nt][e] = (i == i2) ? 1.0 : 0.0;
           }
       }
-      const int64_t row = b * T + F.t0 + ts;
+      const int64_t row = b * T + t0 + ts;
       if (w == 0) {
         if (blog && lane == 0) blog[row] = 1;
         if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
@@ -403,20 +384,154 @@ __global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
       __syncthreads();
       r += 1;
     };
+    // independent row ts (solver.py:305-318, _grow solver.py:368-397)
+    auto grow = [&](const Front& F, int s, int ts) {
+      if (p == ts) {
+        const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
+        const double rinv = 1.0 / F.rsq;  // K = rej / |rej|^2, one rounding more than a division
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+          *reinterpret_cast<double2*>(&S.kv[j0 + 8 * jt + 2 * q]) =
+              make_double2(F.acc[jt][0] * rinv, F.acc[jt][1] * rinv);
+          *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) = As[jt * 32];
+        }
+        if (w == 0) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+            *reinterpret_cast<double2*>(&S.gam[8 * nt + 2 * q]) = make_double2(F.g[nt][0], F.g[nt][1]);
+        }
+      }
+      __syncthreads();
+      // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
+      const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
+      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), F.t0, ts);
+    };
+
+    // Single-row projection of row ts of stage s across the group on the CUDA
+    // cores (solver.py:286-291), for a fresh stream's leading independent rows
+    // (re-projecting the whole tile after each growth costs 64 MMAs per warp).
+    // Leaves gamma, K and the row in the scratch rows; returns |rej|^2, |a|^2.
+    auto project_row = [&](int s, int ts, double& rsq_o, double& asq_o) {
+      const double2* Ar = reinterpret_cast<const double2*>(&S.At[w][s][0][4 * ts + q][0]);
+      double gp[IT], a2 = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) gp[nt] = 0.0;
+#pragma unroll
+      for (int J = 0; J < 4; ++J) {  // my columns j0 + sigma(kt, q) = j0 + 8J + 2q + e
+        const double2 v = Ar[J * 32];
+        a2 = fma(v.x, v.x, fma(v.y, v.y, a2));
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) gp[nt] = fma(Dt[nt][2 * J], v.x, fma(Dt[nt][2 * J + 1], v.y, gp[nt]));
+      }
+      a2 += __shfl_xor_sync(FULL, a2, 1);
+      a2 += __shfl_xor_sync(FULL, a2, 2);
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        gp[nt] += __shfl_xor_sync(FULL, gp[nt], 1);
+        gp[nt] += __shfl_xor_sync(FULL, gp[nt], 2);
+      }
+      // group sums of gamma (per i) and |a|^2 (fixed order)
+      if (q == 0) {
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) S.Gp[w][nt][p][0] = gp[nt];
+        S.red[0][w][p][0] = a2;
+      }
+      __syncthreads();
+      double asq = 0.0;
+#pragma unroll
+      for (int u = 0; u < WG; ++u) asq += S.red[0][u][p][0];
+      // rej_j = a_j - sum_i gamma_i C_ij, j = j0 + 8jt + p, over my rows i = sigma(kt, q)
+      double rp[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int kt = 0; kt < IK; ++kt) {
+        const int i = sigma(kt, q);
+        double gi = 0.0;
+#pragma unroll
+        for (int u = 0; u < WG; ++u) gi += S.Gp[u][i >> 3][i & 7][0];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) rp[jt] = fma(gi, S.Cs[w][kt][jt][lane], rp[jt]);  // Cs = -C
+      }
+      double rej[4], r2 = 0.0;
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) {
+        rp[jt] += __shfl_xor_sync(FULL, rp[jt], 1);
+        rp[jt] += __shfl_xor_sync(FULL, rp[jt], 2);
+        rej[jt] = S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
+        r2 = fma(rej[jt], rej[jt], r2);
+      }
+      r2 += __shfl_xor_sync(FULL, r2, 4);
+      r2 += __shfl_xor_sync(FULL, r2, 8);
+      r2 += __shfl_xor_sync(FULL, r2, 16);
+      if (lane == 0) S.red[1][w][0][0] = r2;
+      __syncthreads();
+      double rsq = 0.0;
+#pragma unroll
+      for (int u = 0; u < WG; ++u) rsq += S.red[1][u][0][0];
+      if (q == 0) {
+        const double rinv = 1.0 / rsq;
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) {
+          S.kv[j0 + 8 * jt + p] = rej[jt] * rinv;
+          S.av[j0 + 8 * jt + p] = S.At[w][s][jt][4 * ts + (p >> 1)][p & 1];
+        }
+        if (w == 0) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            double g = 0.0;
+#pragma unroll
+            for (int u = 0; u < WG; ++u) g += S.Gp[u][nt][p][0];
+            S.gam[8 * nt + p] = g;
+          }
+        }
+      }
+      __syncthreads();
+      rsq_o = rsq;
+      asq_o = asq;
+    };
 
     bool stopped = false;
     int64_t consumed = 0;
     Front F;
+    int64_t tile = 0;
+    int first_row = 0;
     if (ntiles > 0) {
       prefetch(0, 0);
       prefetch(1, 1);
       cp_wait<1>();
-      __syncwarp();
+      __syncthreads();
+      // row mode: a fresh stream's leading independent rows, one at a time
+      if (fresh && !has_x0) {
+        while (tile < ntiles) {
+          const int s = (int)(tile & 1);
+          const int64_t t0 = tile * TT;
+          const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
+          int ts = 0;
+          for (; ts < tv; ++ts) {
+            double rsq, asq;
+            project_row(s, ts, rsq, asq);
+            const double yv = S.Yt[w][s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p] (0 for c >= k)
+            const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
+            if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
+            grow_core(yv, t0, ts);
+          }
+          if (ts < tv) {
+            first_row = ts;
+            break;
+          }
+          consumed = t0 + tv;
+          ++tile;
+          __syncthreads();
+          prefetch(tile + 1, s);
+          cp_wait<1>();
+          __syncthreads();
+        }
+      }
     }
-    for (int64_t tile = 0; tile < ntiles; ++tile) {
+    for (; tile < ntiles; ++tile) {
       const int s = (int)(tile & 1);
-      int row_start = 0;
-      front(tile, s, 0, F);
+      int row_start = first_row;
+      front(tile, s, first_row, F);
+      first_row = 0;
       while (true) {
         if (F.tstar > row_start) scan(F, row_start, F.tstar);
         if (F.tstar >= F.tv) break;
