@@ -38,7 +38,7 @@ struct GroupSmem {
 };
 
 template <int R, int WG>
-__global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
+__global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
     const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
     double* __restrict__ clog) {
@@ -616,35 +616,44 @@ __global__ void __launch_bounds__(WG * 32, 3) blocked_wg_kernel(
 
 }  // namespace blk
 
-namespace {
-constexpr int WGM = 128, WGR = 32, WGW = 4;
-}  // namespace
-
-bool blocked_wg_supports(const rgb_config& cfg) {
-  return cfg.dtype == RGB_F64 && cfg.variant == RGB_GENERAL && cfg.m == WGM && cfg.r_cap == WGR &&
-         cfg.k >= 1 && cfg.k <= 8;
-}
-
-int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
-                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                      cudaStream_t stream, int num_sms) {
-  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
-  auto kern = blk::blocked_wg_kernel<WGR, WGW>;
-  const size_t smem = sizeof(blk::GroupSmem<WGR, WGW>);
+// Instantiations: (r_cap, warps) with m = 32 * warps -- config 3 (m 128,
+// r_cap 32) and config 1 (m 256, r_cap 16, one stream: 8 warps share its work).
+template <int R, int WG>
+static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                     const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                     cudaStream_t stream, int num_sms) {
+  auto kern = blk::blocked_wg_kernel<R, WG>;
+  const size_t smem = sizeof(blk::GroupSmem<R, WG>);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WGW * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WG * 32, smem);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > cfg.num_streams) grid = cfg.num_streams;
-  kern<<<(unsigned)grid, WGW * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                   (const double*)targets, tg_stride, T, logs.branch,
-                                                   (double*)logs.coords);
+  kern<<<(unsigned)grid, WG * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
+                                                  (const double*)targets, tg_stride, T, logs.branch,
+                                                  (double*)logs.coords);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+bool blocked_wg_supports(const rgb_config& cfg) {
+  if (cfg.dtype != RGB_F64 || cfg.variant != RGB_GENERAL || cfg.k < 1 || cfg.k > 8) return false;
+  return (cfg.m == 128 && cfg.r_cap == 32) || (cfg.m == 256 && cfg.r_cap == 16);
+}
+
+int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                      cudaStream_t stream, int num_sms) {
+  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
+  if (cfg.m == 128 && cfg.r_cap == 32)
+    return launch_wg<32, 4>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.m == 256 && cfg.r_cap == 16)
+    return launch_wg<16, 8>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  return RGB_E_UNSUPPORTED;
 }
 
 }  // namespace rgb

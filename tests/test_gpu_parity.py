@@ -57,9 +57,10 @@ def run_batched(rows, targets, *, r_cap, variant="general", eps=None, dtype=torc
 
 # -- golden vectors produced by the reference ------------------------------------
 
-def test_c1_golden_branches_rank_x_pinv(golden):
+@pytest.mark.parametrize("r_cap", [64, 16])  # 64: generic kernel; 16: 8-warp tensor-core kernel
+def test_c1_golden_branches_rank_x_pinv(golden, r_cap):
     g = golden("c1.npz")
-    res = run_batched(g["A"], g["y"], r_cap=64)
+    res = run_batched(g["A"], g["y"], r_cap=r_cap)
     assert int(res["rank"][0]) == int(g["rank"]) == 16
     assert np.array_equal(res["branch"][0], g["branch"])
     assert relerr(res["x"][0, :, 0], g["x"]) <= TOL64
