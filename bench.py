@@ -208,11 +208,16 @@ def cpu_baseline(cfg_name, dtype, rows, tg, reps=1):
     npdt = np.float32 if dtype == "fp32" else np.float64
     rows = rows.astype(npdt, copy=False)
     tg = tg.astype(npdt, copy=False)
+    if rows.shape[0] == 1 and cfg.m * cfg.r > 100000:
+        # single large stream: a bounded prefix (the growth rows plus steady-state
+        # rows at the full rank) keeps the sample to ~10-30 s of CPU work
+        keep = min(rows.shape[1], 2 * cfg.r + 1024)
+        rows, tg = rows[:, :keep], tg[:, :keep]
     S, T, _ = rows.shape
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        oracle.ingest(rows, tg, r_cap=max(cfg.r_cap, 64) if S == 1 else cfg.r_cap, dtype=npdt,
+        oracle.ingest(rows, tg, r_cap=cfg.r_cap, dtype=npdt,
                       nthreads=cores, logs=False)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
@@ -319,19 +324,32 @@ def run_ours(args):
         step()
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # inputs smaller than twice L2 (the single-stream configs): flush L2 between
+    # steps by writing a 512 MB buffer, outside per-step CUDA events
+    in_bytes = (rows.numel() + tg.numel()) * esize
+    flush = in_bytes * world < 2 * 126e6
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=device) if flush else None
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local_dev)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
     t0.record(stream)
     for i in range(args.steps):
-        step(kev[i])
+        if flush:
+            flush_buf.fill_(float(i))
+            sev[i][0].record(stream)
+            step(kev[i])
+            sev[i][1].record(stream)
+        else:
+            step(kev[i])
     t1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     barrier()
     # device time, max over ranks (sharding.py: no collective inside the timed region)
-    elapsed_ms = sharding.max_over_ranks(t0.elapsed_time(t1), device)
+    local_ms = sum(a.elapsed_time(b) for a, b in sev) if flush else t0.elapsed_time(t1)
+    elapsed_ms = sharding.max_over_ranks(local_ms, device)
     kern_ms = sharding.max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in kev), device)
     flops_total = sharding.sum_over_ranks(flops, device)
     n_cap = int(sharding.sum_over_ranks(int((status & 1).astype(bool).sum()), device))
@@ -347,7 +365,7 @@ def run_ours(args):
 
         ns = min(16, S)
         r_np, t_np = rows[:ns].cpu().numpy(), tg[:ns].cpu().numpy()
-        o = oracle.ingest(r_np.astype(np.float64), t_np.astype(np.float64), r_cap=cfg.r_cap if S > 1 else 64,
+        o = oracle.ingest(r_np.astype(np.float64), t_np.astype(np.float64), r_cap=cfg.r_cap,
                           nthreads=8, logs=False)
         x = bs.solution[:ns].cpu().numpy()
         xo = oracle.solution(o)
@@ -398,7 +416,9 @@ def run_ours(args):
             "data": "synthetic: seeded A = G1 G2 per stream generated on device (SURVEY.md 8(d)); inputs resident in HBM",
             "config": {"workload": args.config, "streams": B, "n": n, "m": cfg.m, "rank": cfg.r, "k": cfg.k,
                        "r_cap": cfg.r_cap, "variant": "general", "eps": "auto",
-                       "l2": f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)",
+                       "l2": (f"inputs {in_bytes * world / 1e6:.0f} MB < 2x L2: L2 flushed (512 MB write) between "
+                              "steps, outside the per-step events" if flush else
+                              f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)"),
                        "sharding": f"{S} contiguous streams per GPU, no collective"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,

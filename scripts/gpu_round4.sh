@@ -1,0 +1,3 @@
+set -o pipefail
+for c in c2 c4; do timeout 1200 python bench.py --config $c --steps 1 --warmup 1 --no-e2e 2>&1 | tail -1 > gpurun_out/bench_$c.json; python -c "
+import json; d=json.load(open('gpurun_out/bench_$c.json')); print('$c', 'value %.4g' % d['value'], 'ms/step %.3f' % d['ms_per_step'], 'cpu', d['cpu_baseline'] and d['cpu_baseline']['value'], d['cpu_baseline'] and d['cpu_baseline']['sample'], 'parity', d['parity'])"; done
