@@ -15,6 +15,9 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
                    cudaStream_t stream, int num_sms);
 bool blocked_supports(const rgb_config& cfg);
 bool blocked_wg_supports(const rgb_config& cfg);
+bool grid_supports(const rgb_config& cfg);
+int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
+                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms);
 int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                       const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                       cudaStream_t stream, int num_sms);
@@ -127,6 +130,8 @@ int rgb_ingest(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t r
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
   else if (rgb::blocked_wg_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
+  else if (rgb::grid_supports(*cfg) && !lg.resid && !lg.gain)
+    rc = rgb::launch_grid(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
   if (rc == RGB_E_UNSUPPORTED)
     rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
   if (rc == RGB_E_UNSUPPORTED) return fail(rc, "shape beyond kernel limits (k <= 64, smem)");

@@ -1,0 +1,492 @@
+// rgb_grid.cu -- one large stream on the whole GPU (sm_100a, fp64 tensor cores).
+//
+// For a single stream whose factors are too large for one SM (config 2:
+// m 1024, r 64; config 4: m 2048, r 512) the same 8-row tile algebra as
+// rgb_blocked.cu runs on NC cooperative CTAs (one per SM) separated by grid
+// barriers:
+//
+//   CTA c owns columns [c*CW, (c+1)*CW) of C~ and C (shared memory, MMA
+//   fragment order) and, for c < R/8, the 8-row block c of P^-1 and of W.
+//
+//   P1  G_c = A[:, cols] C~[:, cols]^T (+ a.x0 as 8 extra rows of C~)  -> ws
+//   P2  G   = sum_c G_c (a grid-wide reduction, fixed order)             -> ws
+//   P3  R[:, cols] = A - G C[:, cols]; |R_t|^2 partial                   -> ws
+//   P4  rank test (every CTA, identical); for the dependent rows of the
+//       tile the owners of P compute U_b = P_b G^T and the partials of
+//       S = G P G^T and of G W                                           -> ws
+//   P5  M = I + S = L D L^T, E = L^-1 (every owner, identical);
+//       Y_b = U_b E^T -> ws; W_b += Y_b D^-1 E dy0
+//   P6  P_b -= Y_b D^-1 Y^T  (overlaps P1 of the next tile)
+//
+// five grid barriers per 8 rows instead of three-plus per row for a per-row
+// multi-SM scheme.  An independent row (solver.py:305-318) is applied by
+// every CTA to its own columns / row block, and the rest of its tile is
+// re-projected.  The workspace (partials, barrier counter) is allocated per
+// call with cudaMallocAsync on the caller's stream, so calls stay reentrant.
+#include <cooperative_groups.h>
+
+#include "rgb_mma.cuh"
+
+namespace rgb {
+namespace grd {
+
+using blk::FULL;
+using blk::TT;
+using blk::mma;
+using blk::rcp64;
+
+constexpr int NT = 256;  // threads per CTA (8 warps)
+constexpr int NW = NT / 32;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of the (cooperative) grid; counter zeroed before the launch
+__device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    const unsigned target = epoch * gridDim.x;
+    while (ld_acquire(ctr) < target) __nanosleep(20);
+  }
+  __syncthreads();
+}
+
+template <int R, int CW>
+struct Ws {  // global workspace layout (doubles), per launch
+  static constexpr int GX = R + 8;  // G columns plus 8 for a.x0
+  __host__ __device__ static size_t gpart(int nc) { return (size_t)nc * TT * GX; }
+  static size_t bytes(int nc) {
+    return 256 + sizeof(double) * (gpart(nc) + TT * GX + (size_t)nc * 4 * TT + (size_t)(R / 8) * 2 * 64 +
+                                   (size_t)R * TT + (size_t)R * 8);
+  }
+};
+
+template <int R, int CW>
+struct GridSmem {
+  static constexpr int IT = R / 8, GX = R + 8, GS = R + 20, PS = R + 4, AS = CW + 4;
+  double Ds[(R + 8) / 8][CW / 4][32];  // C~ (and x0^T) of my columns, B-fragment order
+  double Cs[R / 4][CW / 8][32];        // -C of my columns, B-fragment order
+  double Gs[TT][GS];                   // full G of the tile (+ a.x0)
+  double Ps[8][PS];                    // my row block of P^-1
+  double Wb[8][8];                     // my row block of W (c = column)
+  double At[TT][AS];                   // the tile's rows, my columns
+  double Yv[TT][8];                    // targets of the tile
+  double Rs[TT][CW];                   // rejections of my columns
+  double red[NW][TT * (CW > 8 ? CW : 8)];  // per-warp partials (R tile or U_b)
+  double Ub[8][8], Eb[8][8], Dy[8][8], Yb[8][8];
+  double rd[8];
+  double scal[8];
+  int flags[8];
+};
+
+template <int R, int CW>
+__global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state st, const double* __restrict__ rows,
+                                                     int64_t rstride, const double* __restrict__ tgts, int64_t tstride,
+                                                     int64_t T, uint8_t* __restrict__ blog, double* __restrict__ clog,
+                                                     double* __restrict__ ws, unsigned* __restrict__ ctr) {
+  constexpr int IT = R / 8, GX = R + 8, NXT = (R + 8) / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  GridSmem<R, CW>& S = *reinterpret_cast<GridSmem<R, CW>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, p = lane >> 2, q = lane & 3;
+  const int nc = gridDim.x, c = blockIdx.x, c0 = c * CW;
+  const int M = cfg.m, k = cfg.k;
+  const bool owner = c < IT;  // owns row block c of P and W
+  double* ws_g = ws + 32;                          // [nc][TT][GX]
+  double* ws_gf = ws_g + Ws<R, CW>::gpart(nc);     // [TT][GX]
+  double* ws_r0 = ws_gf + TT * GX;                 // [2][nc][2][TT]: |R|^2, |a|^2 partials,
+                                                   // double-buffered by projection parity
+  double* ws_s = ws_r0 + (size_t)nc * 4 * TT;      // [IT][2][64]: S and G W partials
+  double* ws_y = ws_s + (size_t)IT * 2 * 64;       // [R][TT]
+  double* ws_w = ws_y + (size_t)R * TT;            // [R][8]
+  unsigned epoch = 0;
+  unsigned nproj = 0;  // projections so far (selects the ws_r buffer)
+
+  for (int64_t b = 0; b < cfg.num_streams; ++b) {
+    int status = st.status[b];
+    if (status) continue;
+    int r = st.rank[b];
+    const int64_t nobs0 = st.nobs[b];
+    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
+    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
+    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
+    double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
+    const double* Rb = rows + b * rstride;
+    const double* Yb = tgts + b * tstride;
+
+    // ---- load my slices: C~ (+ x0^T as rows R..R+7), -C, my P / W blocks ---------
+    for (int e = tid; e < NXT * (CW / 4) * 32; e += NT) {
+      const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
+      const int i = 8 * nt + (l >> 2), col = c0 + 4 * kt + (l & 3);
+      double v = 0.0;
+      if (i < R) v = Dg[(int64_t)i * M + col];
+      else if (i - R < k) v = Xg[(int64_t)(i - R) * M + col];
+      S.Ds[nt][kt][l] = v;
+    }
+    for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
+      const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
+      S.Cs[kt][nt][l] = -Cg[(int64_t)(4 * kt + (l & 3)) * M + c0 + 8 * nt + (l >> 2)];
+    }
+    if (owner) {
+      for (int e = tid; e < 8 * R; e += NT) S.Ps[e / R][e % R] = Pg[(int64_t)(8 * c + e / R) * R + e % R];
+      for (int e = tid; e < 64; e += NT) S.Wb[e >> 3][e & 7] = 0.0;
+    }
+    __syncthreads();
+
+    const int64_t ntiles = (T + TT - 1) / TT;
+    int64_t consumed = 0;
+    bool stopped = false;
+    for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
+      const int64_t t0 = tile * TT;
+      const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
+      // tile rows of my columns and the targets
+      for (int e = tid; e < TT * CW; e += NT) {
+        const int t = e / CW, j = e % CW;
+        S.At[t][j] = t < tv ? Rb[(t0 + t) * M + c0 + j] : 0.0;
+      }
+      for (int e = tid; e < 64; e += NT) {
+        const int t = e >> 3, cc = e & 7;
+        S.Yv[t][cc] = (t < tv && cc < k) ? Yb[(t0 + t) * k + cc] : 0.0;
+      }
+      __syncthreads();
+      int row_start = 0;
+      while (true) {
+        // a tile whose rows are all independent runs no barrier between the
+        // test's reads of ws_r and the next projection's writes: alternate buffers
+        double* ws_r = ws_r0 + (size_t)(nproj++ & 1u) * nc * 2 * TT;
+        // ---- P1: G partial of my columns (M = t, N = i, K = my columns) -> ws
+        for (int nt = w; nt < NXT; nt += NW) {
+          double acc[2] = {0.0, 0.0};
+#pragma unroll
+          for (int kt = 0; kt < CW / 4; ++kt) mma(acc, S.At[p][4 * kt + q], S.Ds[nt][kt][lane]);
+          *reinterpret_cast<double2*>(ws_g + ((size_t)c * TT + p) * GX + 8 * nt + 2 * q) = make_double2(acc[0], acc[1]);
+        }
+        if (tid < TT) {  // |a_t|^2 of my columns
+          double s = 0.0;
+          for (int j = 0; j < CW; ++j) s = fma(S.At[tid][j], S.At[tid][j], s);
+          ws_r[((size_t)c * 2 + 1) * TT + tid] = s;
+        }
+        grid_sync(ctr, epoch);
+        // ---- P2: G = sum of the partials (elements spread over the grid)
+        for (int e = c * NT + tid; e < TT * GX; e += nc * NT) {
+          double s0 = 0.0, s1 = 0.0;
+          int u = 0;
+          for (; u + 1 < nc; u += 2) {
+            s0 += __ldcg(ws_g + (size_t)u * TT * GX + e);
+            s1 += __ldcg(ws_g + (size_t)(u + 1) * TT * GX + e);
+          }
+          if (u < nc) s0 += __ldcg(ws_g + (size_t)u * TT * GX + e);
+          ws_gf[e] = s0 + s1;
+        }
+        grid_sync(ctr, epoch);
+        for (int e = tid; e < TT * GX; e += NT) S.Gs[e / GX][e % GX] = __ldcg(ws_gf + e);
+        __syncthreads();
+        // ---- P3: R = A - G C on my columns (M = t, N = my columns, K = i split over warps)
+        {
+          double acc[CW / 8][2];
+#pragma unroll
+          for (int nt = 0; nt < CW / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+          const int kmax = (r + 3) >> 2;  // rows of C beyond the rank are zero
+          for (int kt = w; kt < kmax; kt += NW) {
+            const double a = S.Gs[p][4 * kt + q];
+#pragma unroll
+            for (int nt = 0; nt < CW / 8; ++nt) mma(acc[nt], a, S.Cs[kt][nt][lane]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < CW / 8; ++nt) {
+            S.red[w][p * CW + 8 * nt + 2 * q] = acc[nt][0];
+            S.red[w][p * CW + 8 * nt + 2 * q + 1] = acc[nt][1];
+          }
+          __syncthreads();
+          for (int e = tid; e < TT * CW; e += NT) {
+            double v = S.At[e / CW][e % CW];
+#pragma unroll
+            for (int u = 0; u < NW; ++u) v += S.red[u][e];
+            S.Rs[e / CW][e % CW] = v;
+          }
+          __syncthreads();
+          if (tid < TT) {
+            double s = 0.0;
+            for (int j = 0; j < CW; ++j) s = fma(S.Rs[tid][j], S.Rs[tid][j], s);
+            ws_r[((size_t)c * 2) * TT + tid] = s;
+          }
+        }
+        grid_sync(ctr, epoch);
+        // ---- P4: the rank test (identical in every CTA)
+        if (w == 0) {
+          double rsq = 0.0, asq = 0.0;
+          if (lane < TT) {
+            for (int u = 0; u < nc; ++u) {
+              rsq += __ldcg(ws_r + ((size_t)u * 2) * TT + lane);
+              asq += __ldcg(ws_r + ((size_t)u * 2 + 1) * TT + lane);
+            }
+          }
+          bool ybad = false;
+          if (lane < TT)
+            for (int cc = 0; cc < k; ++cc) ybad |= !isfinite(S.Yv[lane][cc]);
+          const bool valid = lane >= row_start && lane < tv;
+          const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
+          const bool bad = !isfinite(asq) || ybad;
+          const unsigned stopm = __ballot_sync(FULL, lane < TT && valid && (!dep || bad));
+          const unsigned badm = __ballot_sync(FULL, lane < TT && valid && bad);
+          if (lane < TT) S.scal[lane] = rsq;
+          if (lane == 0) {
+            S.flags[0] = stopm ? __ffs(stopm) - 1 : tv;
+            S.flags[1] = (int)badm;
+          }
+        }
+        __syncthreads();
+        const int tstar = S.flags[0];
+        const unsigned badm = (unsigned)S.flags[1];
+        if (tstar > row_start) {
+          // ---- dependent rows [row_start, tstar): blocked Sherman-Morrison
+          const int rs = row_start, te = tstar;
+          if (owner) {
+            // U_b = P_b G^T (M = i in my block, N = t, K = i' split over warps)
+            double acc[2] = {0.0, 0.0};
+            const bool in_t = p >= rs && p < te;  // B operand column t = p
+            for (int kt = w; kt < R / 4; kt += NW)
+              mma(acc, S.Ps[p][4 * kt + q], in_t ? S.Gs[p][4 * kt + q] : 0.0);
+            S.red[w][p * 8 + 2 * q] = acc[0];
+            S.red[w][p * 8 + 2 * q + 1] = acc[1];
+            __syncthreads();
+            if (tid < 64) {
+              double v = 0.0;
+#pragma unroll
+              for (int u = 0; u < NW; ++u) v += S.red[u][tid];
+              S.Ub[tid >> 3][tid & 7] = v;
+            }
+            __syncthreads();
+            if (w == 0) {
+              // S_b = G[:, b] U_b and (G W)_b = G[:, b] W_b (M = t, K = i in my block)
+              const bool in_r = p >= rs && p < te;
+              double sp[2] = {0.0, 0.0}, gw[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) {
+                const double a = in_r ? S.Gs[p][8 * c + 4 * kt + q] : 0.0;
+                mma(sp, a, S.Ub[4 * kt + q][p]);
+                mma(gw, a, S.Wb[4 * kt + q][p]);
+              }
+              *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2) * 64 + p * 8 + 2 * q) = make_double2(sp[0], sp[1]);
+              *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2 + 1) * 64 + p * 8 + 2 * q) = make_double2(gw[0], gw[1]);
+            }
+          }
+          grid_sync(ctr, epoch);
+          if (owner) {
+            if (w == 0) {
+              // M = I + S, dy0 = y - a.x0 - G W (acc layout t = p, t' / c = 2q + e)
+              double mi[2] = {0.0, 0.0}, gws[2] = {0.0, 0.0};
+              for (int u = 0; u < IT; ++u) {
+                const double2 s2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q));
+                const double2 g2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q));
+                mi[0] += s2.x;
+                mi[1] += s2.y;
+                gws[0] += g2.x;
+                gws[1] += g2.y;
+              }
+              if (p == 2 * q) mi[0] += 1.0;
+              if (p == 2 * q + 1) mi[1] += 1.0;
+              const bool in_r = p >= rs && p < te;
+#pragma unroll
+              for (int e = 0; e < 2; ++e)  // dy0[t = p][cc = 2q + e]
+                S.Dy[p][2 * q + e] = in_r ? S.Yv[p][2 * q + e] - S.Gs[p][R + 2 * q + e] - gws[e] : 0.0;
+              double ev[2] = {p == 2 * q ? 1.0 : 0.0, p == 2 * q + 1 ? 1.0 : 0.0};
+#pragma unroll
+              for (int kk = 0; kk < TT - 1; ++kk) {
+                const double v = (kk & 1) ? mi[1] : mi[0];
+                const double piv = __shfl_sync(FULL, v, 4 * kk + (kk >> 1));
+                const double mps = __shfl_sync(FULL, v, 4 * p + (kk >> 1));
+                const double m0 = __shfl_sync(FULL, mi[0], 4 * kk + q);
+                const double m1 = __shfl_sync(FULL, mi[1], 4 * kk + q);
+                const double e0 = __shfl_sync(FULL, ev[0], 4 * kk + q);
+                const double e1 = __shfl_sync(FULL, ev[1], 4 * kk + q);
+                const double f = (p > kk) ? mps * rcp64(piv) : 0.0;
+                mi[0] = fma(-f, m0, mi[0]);
+                mi[1] = fma(-f, m1, mi[1]);
+                ev[0] = fma(-f, e0, ev[0]);
+                ev[1] = fma(-f, e1, ev[1]);
+              }
+              S.Eb[p][2 * q] = ev[0];
+              S.Eb[p][2 * q + 1] = ev[1];
+              if ((p >> 1) == q) S.rd[p] = rcp64((p & 1) ? mi[1] : mi[0]);
+              __syncwarp();
+              // Y_b = U_b E^T (M = i, N = t, K = t')
+              double yb[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) mma(yb, S.Ub[p][4 * kt + q], S.Eb[p][4 * kt + q]);
+              S.Yb[p][2 * q] = yb[0];
+              S.Yb[p][2 * q + 1] = yb[1];
+              *reinterpret_cast<double2*>(ws_y + (size_t)(8 * c + p) * TT + 2 * q) = make_double2(yb[0], yb[1]);
+              __syncwarp();
+              // dh = E dy0 (M = t, N = cc, K = t'), scaled by 1/d_t
+              double dh[2] = {0.0, 0.0};
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) mma(dh, S.Eb[p][4 * kt + q], S.Dy[4 * kt + q][p]);
+              S.Dy[p][2 * q] = dh[0] * S.rd[p];
+              S.Dy[p][2 * q + 1] = dh[1] * S.rd[p];
+              __syncwarp();
+              // W_b += Y_b D^-1 E dy0 (M = i, N = cc, K = t)
+              double wb[2] = {S.Wb[p][2 * q], S.Wb[p][2 * q + 1]};
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) mma(wb, S.Yb[p][4 * kt + q], S.Dy[4 * kt + q][p]);
+              S.Wb[p][2 * q] = wb[0];
+              S.Wb[p][2 * q + 1] = wb[1];
+            }
+          }
+          grid_sync(ctr, epoch);
+          if (owner) {
+            // P_b -= Y_b D^-1 Y^T (M = i in my block, N = i', K = t)
+            const double ys0 = -S.Yb[p][q] * S.rd[q], ys1 = -S.Yb[p][4 + q] * S.rd[4 + q];
+            for (int nt = w; nt < IT; nt += NW) {
+              double acc[2] = {S.Ps[p][8 * nt + 2 * q], S.Ps[p][8 * nt + 2 * q + 1]};
+              mma(acc, ys0, __ldcg(ws_y + (size_t)(8 * nt + p) * TT + q));
+              mma(acc, ys1, __ldcg(ws_y + (size_t)(8 * nt + p) * TT + 4 + q));
+              S.Ps[p][8 * nt + 2 * q] = acc[0];
+              S.Ps[p][8 * nt + 2 * q + 1] = acc[1];
+            }
+          }
+          if (c == 0 && tid < TT && tid >= rs && tid < te) {
+            const int64_t row = b * T + t0 + tid;
+            if (blog) blog[row] = 0;
+            if (clog)
+              for (int i = 0; i < R; ++i) clog[row * R + i] = S.Gs[tid][i];
+          }
+          __syncthreads();
+        }
+        if (tstar >= tv) break;
+        if ((badm >> tstar) & 1u) {
+          status |= RGB_ST_NONFINITE;
+          stopped = true;
+          consumed = t0 + tstar;
+          break;
+        }
+        if (r >= R) {
+          status |= RGB_ST_RANK_CAP;
+          stopped = true;
+          consumed = t0 + tstar;
+          break;
+        }
+        // ---- independent row tstar (solver.py:305-318, _grow solver.py:368-397)
+        {
+          const int ts = tstar;
+          const double rinv = 1.0 / S.scal[ts];  // K = rej / |rej|^2 (one rounding more than a division)
+          // C~[:r] -= gamma K^T, C~[r] = K on my columns; C[r] = a
+          for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
+            const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
+            const int i = 8 * nt + (l >> 2), jl = 4 * kt + (l & 3);
+            const double K = S.Rs[ts][jl] * rinv;
+            S.Ds[nt][kt][l] = (i == r) ? K : fma(-S.Gs[ts][i], K, S.Ds[nt][kt][l]);
+          }
+          for (int e = tid; e < CW; e += NT) {
+            const int kt = r >> 2, nt = e >> 3, l = 4 * (e & 7) + (r & 3);
+            S.Cs[kt][nt][l] = -S.At[ts][e];
+          }
+          if (owner) {
+            // P = diag(P, 1); W gains row r = y - a.x0 of row ts
+            for (int e = tid; e < 8 * R; e += NT) {
+              const int i = 8 * c + e / R, i2 = e % R;
+              if (i == r || i2 == r) S.Ps[e / R][i2] = (i == i2) ? 1.0 : 0.0;
+            }
+            if ((r >> 3) == c && tid < 8)
+              S.Wb[r & 7][tid] = tid < k ? S.Yv[ts][tid] - S.Gs[ts][R + tid] : 0.0;
+          }
+          if (c == 0 && tid == 0) {
+            const int64_t row = b * T + t0 + ts;
+            if (blog) blog[row] = 1;
+            if (clog)
+              for (int i = 0; i < R; ++i) clog[row * R + i] = (i == r) ? 1.0 : 0.0;
+          }
+          __syncthreads();
+          r += 1;
+        }
+        row_start = tstar + 1;
+        if (row_start >= tv) break;
+      }
+      if (!stopped) consumed = t0 + tv;
+    }
+
+    // ---- write back: C~, C, P, W -> ws, then x = x0 + C~^T W on my columns ------------
+    for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
+      const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
+      Dg[(int64_t)(8 * nt + (l >> 2)) * M + c0 + 4 * kt + (l & 3)] = S.Ds[nt][kt][l];
+    }
+    for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
+      const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
+      Cg[(int64_t)(4 * kt + (l & 3)) * M + c0 + 8 * nt + (l >> 2)] = -S.Cs[kt][nt][l];
+    }
+    if (owner) {
+      for (int e = tid; e < 8 * R; e += NT) Pg[(int64_t)(8 * c + e / R) * R + e % R] = S.Ps[e / R][e % R];
+      for (int e = tid; e < 64; e += NT) ws_w[(size_t)(8 * c + (e >> 3)) * 8 + (e & 7)] = S.Wb[e >> 3][e & 7];
+    }
+    grid_sync(ctr, epoch);
+    for (int e = tid; e < k * CW; e += NT) {
+      const int cc = e / CW, jl = e % CW;
+      double x = S.Ds[NXT - 1][jl >> 2][4 * (cc) + (jl & 3)];  // x0^T row cc sits in the last N tile
+      // the last N tile of Ds holds x0^T rows R..R+7: lane = 4 * (i - R) + (jl & 3)
+      for (int i = 0; i < r; ++i) x = fma(S.Ds[i >> 3][jl >> 2][4 * (i & 7) + (jl & 3)], __ldcg(ws_w + (size_t)i * 8 + cc), x);
+      Xg[(int64_t)cc * M + c0 + jl] = x;
+    }
+    if (c == 0 && tid == 0) {
+      st.rank[b] = r;
+      st.nobs[b] = nobs0 + consumed;
+      st.status[b] = status;
+    }
+    grid_sync(ctr, epoch);  // the next stream reuses the workspace
+  }
+}
+
+}  // namespace grd
+
+template <int R, int CW>
+static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                         const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                         cudaStream_t stream, int num_sms) {
+  const int nc = cfg.m / CW;
+  if (nc > num_sms || nc < R / 8) return RGB_E_UNSUPPORTED;
+  auto kern = grd::grid_kernel<R, CW>;
+  const size_t smem = sizeof(grd::GridSmem<R, CW>);
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return RGB_E_UNSUPPORTED;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, grd::NT, smem);
+  if (per_sm < 1) return RGB_E_UNSUPPORTED;
+  const size_t wsb = grd::Ws<R, CW>::bytes(nc);
+  void* ws = nullptr;
+  if (cudaMallocAsync(&ws, wsb, stream) != cudaSuccess) return RGB_E_CUDA;
+  cudaMemsetAsync(ws, 0, 256, stream);
+  double* wsd = reinterpret_cast<double*>(ws);
+  unsigned* ctr = reinterpret_cast<unsigned*>(ws);
+  const double* rp = (const double*)rows;
+  const double* tp = (const double*)targets;
+  uint8_t* bl = logs.branch;
+  double* cl = (double*)logs.coords;
+  rgb_config c2 = cfg;
+  rgb_state s2 = st;
+  void* args[] = {&c2, &s2, (void*)&rp, &rows_stride, (void*)&tp, &tg_stride, &T, &bl, &cl, &wsd, &ctr};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(nc), dim3(grd::NT), args, smem, stream);
+  cudaFreeAsync(ws, stream);
+  return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+bool grid_supports(const rgb_config& cfg) {
+  if (cfg.dtype != RGB_F64 || cfg.variant != RGB_GENERAL || cfg.k < 1 || cfg.k > 8) return false;
+  if (cfg.num_streams > 4) return false;  // a handful of large streams, one after the other
+  return (cfg.m == 1024 && cfg.r_cap == 64) || (cfg.m == 2048 && cfg.r_cap == 512);
+}
+
+int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
+                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms) {
+  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
+  if (cfg.m == 1024 && cfg.r_cap == 64)
+    return launch_grid_t<64, 8>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.m == 2048 && cfg.r_cap == 512)
+    return launch_grid_t<512, 16>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  return RGB_E_UNSUPPORTED;
+}
+
+}  // namespace rgb

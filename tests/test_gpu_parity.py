@@ -432,3 +432,24 @@ def test_tensor_core_kernel_agrees_with_generic_kernel(cfg, r_cap):
     for b in np.nonzero(ok)[0][:4]:
         ob = {key: v[b:b + 1] for key, v in o.items() if isinstance(v, np.ndarray)}
         assert relerr(pinv[b], oracle.pinv_closed_form(ob)) <= 1e-9
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", 4096), ("c4", 1200)])
+def test_single_large_stream_grid_kernel(cfg, n):
+    """Configs 2 and 4 (one stream, factors spread over the whole GPU): ranks,
+    branch sequence and x against the oracle; the dual invariant C~ C^T = I."""
+    from paper_2106_11594_b200 import workloads
+
+    A, y = getattr(workloads, cfg)()
+    A, y = A[:n], y[:n]
+    rc = workloads.CONFIGS[cfg].r_cap
+    res = run_batched(A, y, r_cap=rc)
+    o = oracle.ingest(A[None], y[None], r_cap=rc, nthreads=1)
+    assert res["status"][0] == 0 and int(res["rank"][0]) == int(o["rank"][0]) == workloads.CONFIGS[cfg].r
+    assert np.array_equal(res["branch"][0], o["branch"][0])
+    assert relerr(res["x"][0, :, 0], oracle.solution(o)[0, :, 0]) <= 1e-11
+    bs = res["solver"]
+    r = int(res["rank"][0])
+    C = bs.basis_t[0, :r].cpu().numpy()
+    D = bs.dual_t[0, :r].cpu().numpy()
+    assert np.abs(D @ C.T - np.eye(r)).max() <= 1e-9
