@@ -78,7 +78,7 @@ struct GridSmem {
   double At[TT][AS];                   // the tile's rows, my columns
   double Yv[TT][8];                    // targets of the tile
   double Rs[TT][CW];                   // rejections of my columns
-  double red[NW][TT * (CW > 8 ? CW : 8)];  // per-warp partials (R tile or U_b)
+  double red[NW][TT * CW > 128 ? TT * CW : 128];  // per-warp partials
   double Ub[8][8], Eb[8][8], Dy[8][8], Yb[8][8];
   double rd[8];
   double scal[8];
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
   const bool owner = c < IT;  // owns row block c of P and W
   double* ws_g = ws + 32;                          // [nc][TT][GX]
   double* ws_gf = ws_g + Ws<R, CW>::gpart(nc);     // [TT][GX]
-  double* ws_r0 = ws_gf + TT * GX;                 // [2][nc][2][TT]: |R|^2, |a|^2 partials,
+  double* ws_r0 = ws_gf + TT * GX;                 // [2][2][TT][nc]: |R|^2, |a|^2 partials,
                                                    // double-buffered by projection parity
   double* ws_s = ws_r0 + (size_t)nc * 4 * TT;      // [IT][2][64]: S and G W partials
   double* ws_y = ws_s + (size_t)IT * 2 * 64;       // [R][TT]
@@ -169,21 +169,34 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         if (tid < TT) {  // |a_t|^2 of my columns
           double s = 0.0;
           for (int j = 0; j < CW; ++j) s = fma(S.At[tid][j], S.At[tid][j], s);
-          ws_r[((size_t)c * 2 + 1) * TT + tid] = s;
+          ws_r[((size_t)1 * TT + tid) * nc + c] = s;
         }
         grid_sync(ctr, epoch);
-        // ---- P2: G = sum of the partials (elements spread over the grid)
-        for (int e = c * NT + tid; e < TT * GX; e += nc * NT) {
-          double s0 = 0.0, s1 = 0.0;
-          int u = 0;
-          for (; u + 1 < nc; u += 2) {
-            s0 += __ldcg(ws_g + (size_t)u * TT * GX + e);
-            s1 += __ldcg(ws_g + (size_t)(u + 1) * TT * GX + e);
+        // ---- P2: G = sum of the partials.  CTA c reduces a contiguous chunk of
+        // elements: warp w reads partials u = w, w+8, ... (coalesced rows of
+        // 32 elements), then the 8 warp sums are added in a fixed order.
+        {
+          constexpr int NE = TT * GX;
+          const int chunk = (NE + nc - 1) / nc;
+          const int e0 = c * chunk, e1 = (e0 + chunk < NE) ? e0 + chunk : NE;
+          for (int eb = e0; eb < e1; eb += 32) {
+            const int e = eb + lane;
+            double a4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (e < e1) {
+#pragma unroll 4
+              for (int u = w; u < nc; u += NW) a4[(u >> 3) & 3] += __ldcg(ws_g + (size_t)u * NE + e);
+            }
+            S.red[w][lane] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+            __syncthreads();
+            if (w == 0 && e < e1) {
+              double v = 0.0;
+#pragma unroll
+              for (int u = 0; u < NW; ++u) v += S.red[u][lane];
+              ws_gf[e] = v;
+            }
+            __syncthreads();
           }
-          if (u < nc) s0 += __ldcg(ws_g + (size_t)u * TT * GX + e);
-          ws_gf[e] = s0 + s1;
-        }
-        grid_sync(ctr, epoch);
+        }        grid_sync(ctr, epoch);
         for (int e = tid; e < TT * GX; e += NT) S.Gs[e / GX][e % GX] = __ldcg(ws_gf + e);
         __syncthreads();
         // ---- P3: R = A - G C on my columns (M = t, N = my columns, K = i split over warps)
@@ -213,19 +226,30 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           if (tid < TT) {
             double s = 0.0;
             for (int j = 0; j < CW; ++j) s = fma(S.Rs[tid][j], S.Rs[tid][j], s);
-            ws_r[((size_t)c * 2) * TT + tid] = s;
+            ws_r[((size_t)0 * TT + tid) * nc + c] = s;
           }
         }
         grid_sync(ctr, epoch);
-        // ---- P4: the rank test (identical in every CTA)
-        if (w == 0) {
-          double rsq = 0.0, asq = 0.0;
-          if (lane < TT) {
-            for (int u = 0; u < nc; ++u) {
-              rsq += __ldcg(ws_r + ((size_t)u * 2) * TT + lane);
-              asq += __ldcg(ws_r + ((size_t)u * 2 + 1) * TT + lane);
-            }
+        // ---- P4: the rank test (identical in every CTA).  Warp t sums row t's
+        // partials (lane l: CTAs l, l+32, ...; then a fixed butterfly).
+        {
+          double rs_ = 0.0, as_ = 0.0;
+#pragma unroll 4
+          for (int u = lane; u < nc; u += 32) {  // [2][TT][nc]: coalesced
+            rs_ += __ldcg(ws_r + ((size_t)0 * TT + w) * nc + u);
+            as_ += __ldcg(ws_r + ((size_t)1 * TT + w) * nc + u);
           }
+          rs_ = warp_sum(rs_);
+          as_ = warp_sum(as_);
+          if (lane == 0) {
+            S.red[0][w] = rs_;
+            S.red[0][TT + w] = as_;
+          }
+        }
+        __syncthreads();
+        if (w == 0) {
+          const double rsq = lane < TT ? S.red[0][lane] : 0.0;
+          const double asq = lane < TT ? S.red[0][TT + lane] : 0.0;
           bool ybad = false;
           if (lane < TT)
             for (int cc = 0; cc < k; ++cc) ybad |= !isfinite(S.Yv[lane][cc]);
@@ -278,16 +302,30 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
           grid_sync(ctr, epoch);
           if (owner) {
+            {
+              // sums of the S and G W partials: warp w takes owners w, w+8, ...
+              double a4[4] = {0.0, 0.0, 0.0, 0.0};
+              for (int u = w; u < IT; u += NW) {
+                const double2 s2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q));
+                const double2 g2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q));
+                a4[0] += s2.x;
+                a4[1] += s2.y;
+                a4[2] += g2.x;
+                a4[3] += g2.y;
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) S.red[w][4 * lane + i] = a4[i];
+            }
+            __syncthreads();
             if (w == 0) {
               // M = I + S, dy0 = y - a.x0 - G W (acc layout t = p, t' / c = 2q + e)
               double mi[2] = {0.0, 0.0}, gws[2] = {0.0, 0.0};
-              for (int u = 0; u < IT; ++u) {
-                const double2 s2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q));
-                const double2 g2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q));
-                mi[0] += s2.x;
-                mi[1] += s2.y;
-                gws[0] += g2.x;
-                gws[1] += g2.y;
+#pragma unroll
+              for (int u = 0; u < NW; ++u) {
+                mi[0] += S.red[u][4 * lane];
+                mi[1] += S.red[u][4 * lane + 1];
+                gws[0] += S.red[u][4 * lane + 2];
+                gws[1] += S.red[u][4 * lane + 3];
               }
               if (p == 2 * q) mi[0] += 1.0;
               if (p == 2 * q + 1) mi[1] += 1.0;
