@@ -64,6 +64,8 @@ def main():
     ap.add_argument("--key", required=True)
     ap.add_argument("--streams", type=int, required=True, help="streams in the profiled launch")
     ap.add_argument("--rows", type=int, default=1024)
+    ap.add_argument("--alg-bytes-per-row", type=float, default=8 * (64 + 8), help="compulsory bytes per row")
+    ap.add_argument("--job-streams", type=int, default=65536, help="streams of the benchmarked job")
     a = ap.parse_args()
     m = raw_metrics(a.rep)
     pdir = os.path.join(ROOT, "profiles")
@@ -83,9 +85,10 @@ def main():
     summ[a.key] = {
         "source": os.path.basename(a.rep), "profiled_streams": a.streams, "rows": a.rows,
         "dram_bytes_profiled_launch": rd + wr, "dram_bytes_per_row": per_row,
-        "algorithmic_bytes_per_row": 8 * (64 + 8),
-        "note": "dram_bytes_per_launch scales the per-row traffic of the profiled launch to 65536 streams",
-        "dram_bytes_per_launch": per_row * 65536 * a.rows,
+        "algorithmic_bytes_per_row": a.alg_bytes_per_row,
+        "traffic_over_compulsory": per_row / a.alg_bytes_per_row,
+        "note": f"dram_bytes_per_launch scales the per-row traffic of the profiled launch to {a.job_streams} streams",
+        "dram_bytes_per_launch": per_row * a.job_streams * a.rows,
         "dmma_pipe_pct": m.get("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", ["?"])[0],
         "registers": m.get("launch__registers_per_thread", ["?"])[0],
         "warps_active_per_sm": m.get("sm__warps_active.avg.per_cycle_active", ["?"])[0],
