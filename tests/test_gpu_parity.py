@@ -453,3 +453,74 @@ def test_single_large_stream_grid_kernel(cfg, n):
     C = bs.basis_t[0, :r].cpu().numpy()
     D = bs.dual_t[0, :r].cpu().numpy()
     assert np.abs(D @ C.T - np.eye(r)).max() <= 1e-9
+
+
+def _shape_rows(cfg, streams, n, rank_extra=0):
+    """Rows of a config's shape; rank_extra > 0 appends independent rows so
+    that the rank exceeds the device capacity."""
+    from paper_2106_11594_b200 import workloads
+
+    if cfg in ("c5", "c3"):
+        rows, tg = workloads.host_batch(cfg, streams, n=n)
+    else:
+        A, y = getattr(workloads, cfg)()
+        rows, tg = A[None, :n], y[None, :n, None]
+    if rank_extra:
+        rng = np.random.default_rng(11)
+        rows = rows.copy()
+        rows[:, n // 2: n // 2 + rank_extra] = rng.standard_normal((rows.shape[0], rank_extra, rows.shape[2]))
+    return np.ascontiguousarray(rows), np.ascontiguousarray(tg)
+
+
+KERNEL_SHAPES = [("c5", 16, [0, 1, 2]), ("c3", 32, [0, 1]), ("c2", 64, [0])]
+
+
+@pytest.mark.parametrize("cfg,r_cap,streams", KERNEL_SHAPES)
+def test_partial_tiles_and_single_row_calls(cfg, r_cap, streams):
+    """Row counts that are not multiples of the 8-row tile, and one-row calls
+    (the update() pattern), give the one-shot result on every tensor-core kernel."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    rows, tg = _shape_rows(cfg, streams, 77)
+    B, n, m = rows.shape
+    one = run_batched(rows, tg, r_cap=r_cap, logs=False)
+    bs = BatchedSolver(B, m, k=tg.shape[2], r_cap=r_cap)
+    lo = 0
+    for hi in (1, 2, 13, 30, 31, 77):
+        bs.ingest(dev(np.ascontiguousarray(rows[:, lo:hi])), dev(np.ascontiguousarray(tg[:, lo:hi])))
+        lo = hi
+    torch.cuda.synchronize()
+    assert np.array_equal(bs.rank.cpu().numpy(), one["rank"])
+    assert (bs.nobs_t.cpu().numpy() == n).all()
+    X = bs.solution.cpu().numpy()
+    for b in range(B):
+        assert relerr(X[b], one["x"][b]) <= 1e-11
+
+
+@pytest.mark.parametrize("cfg,r_cap,streams", KERNEL_SHAPES)
+def test_nonfinite_row_freezes_stream_on_tensor_core_kernels(cfg, r_cap, streams):
+    rows, tg = _shape_rows(cfg, streams, 50)
+    rows = rows.copy()
+    bad_row = 29  # mid-tile
+    rows[0, bad_row, 3] = np.nan
+    res = run_batched(rows, tg, r_cap=r_cap)
+    assert res["status"][0] & 2 and int(res["nobs"][0]) == bad_row
+    o = oracle.ingest(rows[:1, :bad_row], tg[:1, :bad_row], r_cap=r_cap)
+    assert int(res["rank"][0]) == int(o["rank"][0])
+    assert relerr(res["x"][0], oracle.solution(o)[0]) <= 1e-10
+    for b in range(1, rows.shape[0]):
+        assert res["status"][b] == 0 and int(res["nobs"][b]) == 50
+
+
+@pytest.mark.parametrize("cfg,r_cap,streams", [("c5", 16, [0, 1]), ("c3", 32, [0])])
+def test_rank_capacity_freezes_stream_on_tensor_core_kernels(cfg, r_cap, streams):
+    """A stream whose rank would exceed r_cap stops at that row with
+    RGB_ST_RANK_CAP (the reference would grow; the drop-in RecursiveSolver
+    grows the capacity instead)."""
+    rows, tg = _shape_rows(cfg, streams, 120, rank_extra=r_cap + 4)
+    res = run_batched(rows, tg, r_cap=r_cap)
+    o = oracle.ingest(rows, tg, r_cap=r_cap)
+    assert np.array_equal(res["status"] & 1, o["status"] & 1)
+    assert (res["status"] & 1).all()
+    assert np.array_equal(res["nobs"], o["nobs"])
+    assert (res["rank"] == r_cap).all()
