@@ -67,7 +67,9 @@ struct WarpSmem {
 #define RGB_BLOCKED_MINB 3
 #endif
 
-template <int M, int R, int KC, int WARPS>
+// GEN: general variant only (the headline instantiation); !GEN: orthogonal /
+// orthonormal, whose grow step differs (solver.py:382-395)
+template <int M, int R, int KC, int WARPS, bool GEN>
 __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
     const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
@@ -270,7 +272,9 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
             const double2 v = As[jt * 32];
             *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
                 make_double2(X.acc[jt][0] * rinv, X.acc[jt][1] * rinv);
-            *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) = v;
+            // the row itself (general: C[r] = a) or its rejection (other variants)
+            *reinterpret_cast<double2*>(&S.u.ind.av[8 * jt + 2 * q]) =
+                GEN ? v : make_double2(X.acc[jt][0], X.acc[jt][1]);
           }
         }
         __syncwarp();
@@ -458,50 +462,136 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // independent row ts of front F (solver.py:305-318, _grow solver.py:368-397)
     // grow_core: the independent-row update from the scratch rows written by
     // front_end() or project_row(); wnew = y - a.x0 of the row for RHS c = p
-    auto grow_core = [&](double wnew, int64_t t0, int ts) {
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (8 * nt + 2 * q + e == r) Wt[nt][e] = wnew;
-      // C~[:r] -= gamma K^T, C~[r] = K   (solver.py:377-380)
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt) {
-        const int i = 8 * nt + p;
-        const double gi = S.u.ind.gam[i];
-#pragma unroll
-        for (int J = 0; J < JK / 2; ++J) {
-          const double2 kv = *reinterpret_cast<const double2*>(&S.u.ind.kv[8 * J + 2 * q]);
-          Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
-          Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
-        }
-      }
-      // C[r] = a  (solver.py:376)
-      if (q == ((r & 7) >> 1)) {
-        const int ktr = 2 * (r >> 3) + (r & 1);
-#pragma unroll
-        for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = -S.u.ind.av[8 * jt + p];
-      }
-      // P = diag(P, 1)  (solver.py:372-373, 381)
-#pragma unroll
-      for (int mt = 0; mt < IT; ++mt)
+    auto grow_core = [&](double wnew, double rsq, int64_t t0, int ts) {
+      const int var = GEN ? RGB_GENERAL : cfg.variant;
+      double last = 1.0;  // coords_row[r] of the orthogonal / orthonormal variants
+      if (var == RGB_GENERAL) {
+        // W gains row r: y - a.x0 (x = x0 + C~^T W stays exact)
 #pragma unroll
         for (int nt = 0; nt < IT; ++nt)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
-            if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
+          for (int e = 0; e < 2; ++e)
+            if (8 * nt + 2 * q + e == r) Wt[nt][e] = wnew;
+        // C~[:r] -= gamma K^T, C~[r] = K   (solver.py:377-380)
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          const int i = 8 * nt + p;
+          const double gi = S.u.ind.gam[i];
+#pragma unroll
+          for (int J = 0; J < JK / 2; ++J) {
+            const double2 kv = *reinterpret_cast<const double2*>(&S.u.ind.kv[8 * J + 2 * q]);
+            Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
+            Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
           }
+        }
+        // C[r] = a  (solver.py:376)
+        if (q == ((r & 7) >> 1)) {
+          const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = -S.u.ind.av[8 * jt + p];
+        }
+        // P = diag(P, 1)  (solver.py:372-373, 381)
+#pragma unroll
+        for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
+              if (i == r || i2 == r) Pr[mt][nt][e] = (i == i2) ? 1.0 : 0.0;
+            }
+      } else {
+        // orthogonal / orthonormal _grow (solver.py:382-395); av holds the rejection.
+        // z = P gamma, denom = 1 + gamma.z (solver.py:307-310)
+        double z[IT];
+#pragma unroll
+        for (int mt = 0; mt < IT; ++mt) {
+          double zp = 0.0;
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) zp = fma(Pr[mt][nt][e], S.u.ind.gam[8 * nt + 2 * q + e], zp);
+          zp += __shfl_xor_sync(FULL, zp, 1);
+          zp += __shfl_xor_sync(FULL, zp, 2);
+          z[mt] = zp;  // z[8mt + p]
+        }
+        double dn = 0.0;
+        if (q == 0) {
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt) dn = fma(S.u.ind.gam[8 * mt + p], z[mt], dn);
+        }
+        const double denom = 1.0 + warp_sum(dn);
+        // rescaling (solver.py:354-366, 383): alpha = 1/(1/rescale)
+        const double resc = (var == RGB_ORTHONORMAL) ? 1.0 / sqrt(rsq) : cfg.alpha;
+        last = 1.0 / resc;
+        const double alpha = 1.0 / last;
+        // W gains row r: alpha (y - a.x) with a.x = a.x0 + gamma^T W, since the
+        // new dual row is K / alpha and the old dual rows do not move
+        double gw = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) gw = fma(S.u.ind.gam[8 * nt + 2 * q + e], Wt[nt][e], gw);
+        gw += __shfl_xor_sync(FULL, gw, 1);
+        gw += __shfl_xor_sync(FULL, gw, 2);
+        const double wr = alpha * (wnew - gw);
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (8 * nt + 2 * q + e == r) Wt[nt][e] = wr;
+        __syncwarp();
+        if (q == 0) {
+#pragma unroll
+          for (int mt = 0; mt < IT; ++mt) S.u.ind.kv[8 * mt + p] = z[mt];  // kv is free: C~[:r] is unchanged
+        }
+        __syncwarp();
+        // C[r] = alpha rej;  C~[r] = rej / (alpha |rej|^2)  (orthonormal: C~ is C)
+        if (q == ((r & 7) >> 1)) {
+          const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) S.Cs[ktr][jt][lane] = -(alpha * S.u.ind.av[8 * jt + p]);
+        }
+        const double sc = alpha * rsq;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          if (8 * nt + p == r) {
+#pragma unroll
+            for (int J = 0; J < JK / 2; ++J)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const double rj = S.u.ind.av[8 * J + 2 * q + e];
+                Dt[nt][2 * J + e] = (var == RGB_ORTHONORMAL) ? alpha * rj : rj / sc;
+              }
+          }
+        }
+        // P gains edge -alpha z and corner alpha^2 denom
+#pragma unroll
+        for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
+              if (i == r && i2 == r) Pr[mt][nt][e] = alpha * alpha * denom;
+              else if (i2 == r) Pr[mt][nt][e] = (i < r) ? -(alpha * S.u.ind.kv[i]) : 0.0;
+              else if (i == r) Pr[mt][nt][e] = (i2 < r) ? -(alpha * S.u.ind.kv[i2]) : 0.0;
+            }
+      }
       const int64_t row = b * T + t0 + ts;
       if (blog && lane == 0) blog[row] = 1;
-      if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
+      if (clog && lane < R) {
+        double v = (lane == r) ? 1.0 : 0.0;
+        if (var != RGB_GENERAL) v = (lane < r) ? S.u.ind.gam[lane] : (lane == r ? last : 0.0);
+        clog[row * R + lane] = v;
+      }
       __syncwarp();
       r += 1;
     };
     auto grow = [&](const Front& F, int ts) {
       // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
       const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
-      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), F.t0, ts);
+      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), GEN ? 0.0 : __shfl_sync(FULL, F.rsq, 4 * ts), F.t0, ts);
     };
 
     // Single-row projection of row ts of stage s on the current basis, on the
@@ -561,7 +651,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
           S.u.ind.kv[8 * jt + p] = rej[jt] * rinv;
-          S.u.ind.av[8 * jt + p] = S.At[s][jt][4 * ts + (p >> 1)][p & 1];
+          S.u.ind.av[8 * jt + p] = GEN ? S.At[s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
         }
       }
       __syncwarp();
@@ -590,7 +680,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
             const double yv = S.Yt[s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p]
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
             if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
-            grow_core(yv, t0, ts);
+            grow_core(yv, rsq, t0, ts);
           }
           if (ts < tv) {
             first_row = ts;
@@ -716,20 +806,24 @@ constexpr int BWARPS = RGB_BLOCKED_WARPS;
 }  // namespace
 
 bool blocked_supports(const rgb_config& cfg) {
-  return cfg.dtype == RGB_F64 && cfg.variant == RGB_GENERAL && cfg.m == BM && cfg.r_cap == BR &&
-         cfg.k == BK;
+  // all three variants; a zero orthogonal rescaling factor (an error in the
+  // reference, solver.py:364-365) is left to the generic kernel's status path
+  const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
+                      (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
+  return cfg.dtype == RGB_F64 && var_ok && cfg.m == BM && cfg.r_cap == BR && cfg.k == BK;
 }
 
 int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms) {
   if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;  // per-row residuals: generic kernel
-  auto kern = blk::blocked_kernel<BM, BR, BK, BWARPS>;
+  const bool gen = cfg.variant == RGB_GENERAL;
+  auto kern = gen ? blk::blocked_kernel<BM, BR, BK, BWARPS, true> : blk::blocked_kernel<BM, BR, BK, BWARPS, false>;
   const size_t smem = sizeof(blk::WarpSmem<BM, BR, BK>) * BWARPS;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[2] = {false, false};
+  if (!attr[gen]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[gen] = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BWARPS * 32, smem);

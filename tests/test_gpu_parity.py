@@ -25,7 +25,7 @@ def dev(a, dtype=torch.float64):
 
 
 def run_batched(rows, targets, *, r_cap, variant="general", eps=None, dtype=torch.float64, logs=True,
-                resid=False):
+                resid=False, alpha=1.0):
     """Batched ingest through librgb.so.  `logs` requests the branch and coords
     logs (supported by every kernel); `resid` additionally requests per-row
     residuals, which only the generic kernel writes (so it forces that kernel)."""
@@ -39,7 +39,7 @@ def run_batched(rows, targets, *, r_cap, variant="general", eps=None, dtype=torc
         targets = targets[..., None]
     B, T, m = rows.shape
     k = targets.shape[-1]
-    bs = BatchedSolver(B, m, k=k, r_cap=r_cap, variant=variant, eps=eps, dtype=dtype)
+    bs = BatchedSolver(B, m, k=k, r_cap=r_cap, variant=variant, eps=eps, dtype=dtype, alpha=alpha)
     out = {}
     if logs:
         out["branch"] = torch.zeros((B, T), dtype=torch.uint8, device="cuda")
@@ -206,8 +206,10 @@ def ambiguous_rows(rho):
     return (rho >= 0.125) & (rho <= 8.0)
 
 
-def compare_to_oracle(rows, targets, res, r_cap, tol=TOL64, variant="general"):
-    o = oracle.ingest(rows, targets, r_cap=r_cap, variant=variant, nthreads=8)
+def compare_to_oracle(rows, targets, res, r_cap, tol=TOL64, variant="general", alpha=1.0, out=None):
+    o = oracle.ingest(rows, targets, r_cap=r_cap, variant=variant, alpha=alpha, nthreads=8)
+    if out is not None:
+        out.update(o)
     amb_rows = ambiguous_rows(o["rho"])
     amb = amb_rows.any(axis=1) | (o["status"] != 0) | (res["status"] != 0)
     ok = ~amb
@@ -524,3 +526,34 @@ def test_rank_capacity_freezes_stream_on_tensor_core_kernels(cfg, r_cap, streams
     assert (res["status"] & 1).all()
     assert np.array_equal(res["nobs"], o["nobs"])
     assert (res["rank"] == r_cap).all()
+
+
+@pytest.mark.parametrize("variant,alpha", [("orthogonal", 1.0), ("orthogonal", 0.37), ("orthonormal", 1.0)])
+def test_variants_on_tensor_core_kernel(variant, alpha):
+    """Orthogonal / orthonormal factorisations (solver.py:382-395) through the
+    one-warp tensor-core kernel (config-5 shape): branches, ranks and x against
+    the oracle; the stored factors C, C~, P^-1 and the coords log (gamma, 1/alpha)
+    against the oracle's; agreement with the generic kernel; A+ from the log."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch("c5", list(range(48)), n=1024)
+    res = run_batched(rows, tg, r_cap=16, variant=variant, alpha=alpha)
+    o = {}
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16, variant=variant, alpha=alpha, out=o)
+    assert amb <= 2 and worst <= 1e-10, (amb, worst)
+    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (res["status"] != 0))
+    bs = res["solver"]
+    C, D, P = (t.cpu().numpy() for t in (bs.basis_t, bs.dual_t, bs.gram_t))
+    for b in np.nonzero(ok)[0]:
+        assert relerr(C[b], o["C"][b]) <= 1e-10
+        assert relerr(D[b], o["C"][b] if variant == "orthonormal" else o["D"][b]) <= 1e-10
+        assert relerr(P[b], o["P"][b]) <= 1e-9
+        assert relerr(res["coords"][b], o["coords"][b]) <= 1e-9
+    gen = run_batched(rows, tg, r_cap=16, variant=variant, alpha=alpha, resid=True)
+    assert np.array_equal(gen["branch"][ok], res["branch"][ok])
+    for b in np.nonzero(ok)[0]:
+        assert relerr(res["x"][b], gen["x"][b]) <= 1e-11
+    pinv = bs.pinv(dev(res["coords"])).cpu().numpy()
+    for b in np.nonzero(ok)[0][:4]:
+        ob = {key: v[b:b + 1] for key, v in o.items() if isinstance(v, np.ndarray)}
+        assert relerr(pinv[b], oracle.pinv_closed_form(ob, variant=variant)) <= 1e-9
