@@ -37,7 +37,8 @@ struct GroupSmem {
   double av[M];                      //                  the row
 };
 
-template <int R, int WG>
+// GEN: general variant only; !GEN: orthogonal / orthonormal (solver.py:382-395)
+template <int R, int WG, bool GEN>
 __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
     const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
@@ -342,44 +343,120 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     };
 
     // the update itself, from the scratch rows (gam, kv, av)
-    auto grow_core = [&](double wnew, int64_t t0, int ts) {
-      if (w == (r >> 3)) {
+    auto grow_core = [&](double wnew, double rsq, int64_t t0, int ts) {
+      const int var = GEN ? RGB_GENERAL : cfg.variant;
+      double last = 1.0;  // coords_row[r] of the orthogonal / orthonormal variants
+      if (var == RGB_GENERAL) {
+        if (w == (r >> 3)) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (8 * w + 2 * q + e == r) Wt[e] = wnew;
-      }
-      // C~[:r] -= gamma K^T, C~[r] = K on the own columns (solver.py:377-380)
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt) {
-        const int i = 8 * nt + p;
-        const double gi = S.gam[i];
-#pragma unroll
-        for (int J = 0; J < 4; ++J) {
-          const double2 kv = *reinterpret_cast<const double2*>(&S.kv[j0 + 8 * J + 2 * q]);
-          Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
-          Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
+          for (int e = 0; e < 2; ++e)
+            if (8 * w + 2 * q + e == r) Wt[e] = wnew;
         }
-      }
-      // C[r] = a
-      if (q == ((r & 7) >> 1)) {
-        const int ktr = 2 * (r >> 3) + (r & 1);
+        // C~[:r] -= gamma K^T, C~[r] = K on the own columns (solver.py:377-380)
 #pragma unroll
-        for (int jt = 0; jt < 4; ++jt) S.Cs[w][ktr][jt][lane] = -S.av[j0 + 8 * jt + p];
-      }
-      // P = diag(P, 1)
-      if (w < IT) {
+        for (int nt = 0; nt < IT; ++nt) {
+          const int i = 8 * nt + p;
+          const double gi = S.gam[i];
 #pragma unroll
-        for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = 8 * w + p, i2 = 8 * nt + 2 * q + e;
-            if (i == r || i2 == r) Pr[nt][e] = (i == i2) ? 1.0 : 0.0;
+          for (int J = 0; J < 4; ++J) {
+            const double2 kv = *reinterpret_cast<const double2*>(&S.kv[j0 + 8 * J + 2 * q]);
+            Dt[nt][2 * J] = (i == r) ? kv.x : fma(-gi, kv.x, Dt[nt][2 * J]);
+            Dt[nt][2 * J + 1] = (i == r) ? kv.y : fma(-gi, kv.y, Dt[nt][2 * J + 1]);
           }
+        }
+        // C[r] = a
+        if (q == ((r & 7) >> 1)) {
+          const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt) S.Cs[w][ktr][jt][lane] = -S.av[j0 + 8 * jt + p];
+        }
+        // P = diag(P, 1)
+        if (w < IT) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * w + p, i2 = 8 * nt + 2 * q + e;
+              if (i == r || i2 == r) Pr[nt][e] = (i == i2) ? 1.0 : 0.0;
+            }
+        }
+      } else {
+        // orthogonal / orthonormal _grow (solver.py:382-395); av holds the rejection.
+        // z = P gamma (rows 8w + p), gamma^T W (column p) partials of warp w
+        double z = 0.0, gw = 0.0;
+        if (w < IT) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) z = fma(Pr[nt][e], S.gam[8 * nt + 2 * q + e], z);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) gw = fma(S.gam[8 * w + 2 * q + e], Wt[e], gw);
+          z += __shfl_xor_sync(FULL, z, 1);
+          z += __shfl_xor_sync(FULL, z, 2);
+          gw += __shfl_xor_sync(FULL, gw, 1);
+          gw += __shfl_xor_sync(FULL, gw, 2);
+          if (q == 0) {
+            S.kv[8 * w + p] = z;  // kv is free: C~[:r] is unchanged
+            S.red[2][w][p][0] = gw;
+          }
+        }
+        __syncthreads();
+        double dn = 0.0, gws = 0.0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) dn = fma(S.gam[i], S.kv[i], dn);
+#pragma unroll
+        for (int u = 0; u < IT; ++u) gws += S.red[2][u][p][0];
+        const double denom = 1.0 + dn;  // solver.py:307-310
+        const double resc = (var == RGB_ORTHONORMAL) ? 1.0 / sqrt(rsq) : cfg.alpha;
+        last = 1.0 / resc;
+        const double alpha = 1.0 / last;
+        // W gains row r: alpha (y - a.x), the new dual row being K / alpha
+        if (w == (r >> 3)) {
+          const double wr = alpha * (wnew - gws);
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (8 * w + 2 * q + e == r) Wt[e] = wr;
+        }
+        // C[r] = alpha rej;  C~[r] = rej / (alpha |rej|^2)  (orthonormal: C~ is C)
+        if (q == ((r & 7) >> 1)) {
+          const int ktr = 2 * (r >> 3) + (r & 1);
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt) S.Cs[w][ktr][jt][lane] = -(alpha * S.av[j0 + 8 * jt + p]);
+        }
+        const double sc = alpha * rsq;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          if (8 * nt + p == r) {
+#pragma unroll
+            for (int J = 0; J < 4; ++J)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const double rj = S.av[j0 + 8 * J + 2 * q + e];
+                Dt[nt][2 * J + e] = (var == RGB_ORTHONORMAL) ? alpha * rj : rj / sc;
+              }
+          }
+        }
+        // P gains edge -alpha z and corner alpha^2 denom
+        if (w < IT) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * w + p, i2 = 8 * nt + 2 * q + e;
+              if (i == r && i2 == r) Pr[nt][e] = alpha * alpha * denom;
+              else if (i2 == r) Pr[nt][e] = (i < r) ? -(alpha * S.kv[i]) : 0.0;
+              else if (i == r) Pr[nt][e] = (i2 < r) ? -(alpha * S.kv[i2]) : 0.0;
+            }
+        }
       }
       const int64_t row = b * T + t0 + ts;
       if (w == 0) {
         if (blog && lane == 0) blog[row] = 1;
-        if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
+        if (clog && lane < R) {
+          double v = (lane == r) ? 1.0 : 0.0;
+          if (var != RGB_GENERAL) v = (lane < r) ? S.gam[lane] : (lane == r ? last : 0.0);
+          clog[row * R + lane] = v;
+        }
       }
       __syncthreads();
       r += 1;
@@ -393,7 +470,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         for (int jt = 0; jt < 4; ++jt) {
           *reinterpret_cast<double2*>(&S.kv[j0 + 8 * jt + 2 * q]) =
               make_double2(F.acc[jt][0] * rinv, F.acc[jt][1] * rinv);
-          *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) = As[jt * 32];
+          // the row itself (general: C[r] = a) or its rejection (other variants)
+          *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) =
+              GEN ? As[jt * 32] : make_double2(F.acc[jt][0], F.acc[jt][1]);
         }
         if (w == 0) {
 #pragma unroll
@@ -404,7 +483,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       __syncthreads();
       // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
       const double dv = (ts & 1) ? F.dyx[1] : F.dyx[0];
-      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), F.t0, ts);
+      grow_core(__shfl_sync(FULL, dv, 4 * p + (ts >> 1)), GEN ? 0.0 : __shfl_sync(FULL, F.rsq, 4 * ts), F.t0, ts);
     };
 
     // Single-row projection of row ts of stage s across the group on the CUDA
@@ -472,7 +551,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt) {
           S.kv[j0 + 8 * jt + p] = rej[jt] * rinv;
-          S.av[j0 + 8 * jt + p] = S.At[w][s][jt][4 * ts + (p >> 1)][p & 1];
+          S.av[j0 + 8 * jt + p] = GEN ? S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
         }
         if (w == 0) {
 #pragma unroll
@@ -512,7 +591,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
             const double yv = S.Yt[w][s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p] (0 for c >= k)
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
             if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
-            grow_core(yv, t0, ts);
+            grow_core(yv, rsq, t0, ts);
           }
           if (ts < tv) {
             first_row = ts;
@@ -622,12 +701,13 @@ template <int R, int WG>
 static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                      cudaStream_t stream, int num_sms) {
-  auto kern = blk::blocked_wg_kernel<R, WG>;
+  const bool gen = cfg.variant == RGB_GENERAL;
+  auto kern = gen ? blk::blocked_wg_kernel<R, WG, true> : blk::blocked_wg_kernel<R, WG, false>;
   const size_t smem = sizeof(blk::GroupSmem<R, WG>);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[2] = {false, false};
+  if (!attr[gen]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    attr[gen] = true;
   }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WG * 32, smem);
@@ -641,7 +721,9 @@ static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int
 }
 
 bool blocked_wg_supports(const rgb_config& cfg) {
-  if (cfg.dtype != RGB_F64 || cfg.variant != RGB_GENERAL || cfg.k < 1 || cfg.k > 8) return false;
+  const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
+                      (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
+  if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
   return (cfg.m == 128 && cfg.r_cap == 32) || (cfg.m == 256 && cfg.r_cap == 16);
 }
 

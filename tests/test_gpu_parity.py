@@ -68,6 +68,22 @@ def test_c1_golden_branches_rank_x_pinv(golden, r_cap):
     assert relerr(pinv, g["pinv"]) <= TOL64
 
 
+@pytest.mark.parametrize("variant,alpha", [("orthogonal", 2.5), ("orthonormal", 1.0)])
+def test_c1_variants_on_warp_group_kernel(golden, variant, alpha):
+    """Config 1 (m 256, rank 16) through the 8-warp tensor-core kernel with the
+    orthogonal / orthonormal factorisations: the reference's branch sequence and
+    x, and A+ from the coords log, against the oracle's closed form."""
+    g = golden("c1.npz")
+    res = run_batched(g["A"], g["y"], r_cap=16, variant=variant, alpha=alpha)
+    assert int(res["rank"][0]) == 16
+    assert np.array_equal(res["branch"][0], g["branch"])
+    assert relerr(res["x"][0, :, 0], g["x"]) <= TOL64
+    o = oracle.ingest(g["A"], g["y"], r_cap=16, variant=variant, alpha=alpha)
+    assert relerr(res["coords"][0], o["coords"][0]) <= 1e-9
+    pinv = res["solver"].pinv(dev(res["coords"])).cpu().numpy()[0]
+    assert relerr(pinv, g["pinv"]) <= TOL64
+
+
 @pytest.mark.parametrize("name,r_cap", [("c5_sample.npz", 16), ("c3_sample.npz", 32)])
 def test_batched_golden_samples(golden, name, r_cap):
     g = golden(name)
@@ -528,18 +544,20 @@ def test_rank_capacity_freezes_stream_on_tensor_core_kernels(cfg, r_cap, streams
     assert (res["rank"] == r_cap).all()
 
 
+@pytest.mark.parametrize("cfg,r_cap,n", [("c5", 16, 1024), ("c3", 32, 512)])
 @pytest.mark.parametrize("variant,alpha", [("orthogonal", 1.0), ("orthogonal", 0.37), ("orthonormal", 1.0)])
-def test_variants_on_tensor_core_kernel(variant, alpha):
+def test_variants_on_tensor_core_kernel(cfg, r_cap, n, variant, alpha):
     """Orthogonal / orthonormal factorisations (solver.py:382-395) through the
-    one-warp tensor-core kernel (config-5 shape): branches, ranks and x against
+    one-warp (config-5 shape) and warp-group (config-3 shape) tensor-core
+    kernels: branches, ranks and x against
     the oracle; the stored factors C, C~, P^-1 and the coords log (gamma, 1/alpha)
     against the oracle's; agreement with the generic kernel; A+ from the log."""
     from paper_2106_11594_b200 import workloads
 
-    rows, tg = workloads.host_batch("c5", list(range(48)), n=1024)
-    res = run_batched(rows, tg, r_cap=16, variant=variant, alpha=alpha)
+    rows, tg = workloads.host_batch(cfg, list(range(48)), n=n)
+    res = run_batched(rows, tg, r_cap=r_cap, variant=variant, alpha=alpha)
     o = {}
-    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16, variant=variant, alpha=alpha, out=o)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=r_cap, variant=variant, alpha=alpha, out=o)
     assert amb <= 2 and worst <= 1e-10, (amb, worst)
     ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (res["status"] != 0))
     bs = res["solver"]
@@ -549,7 +567,7 @@ def test_variants_on_tensor_core_kernel(variant, alpha):
         assert relerr(D[b], o["C"][b] if variant == "orthonormal" else o["D"][b]) <= 1e-10
         assert relerr(P[b], o["P"][b]) <= 1e-9
         assert relerr(res["coords"][b], o["coords"][b]) <= 1e-9
-    gen = run_batched(rows, tg, r_cap=16, variant=variant, alpha=alpha, resid=True)
+    gen = run_batched(rows, tg, r_cap=r_cap, variant=variant, alpha=alpha, resid=True)
     assert np.array_equal(gen["branch"][ok], res["branch"][ok])
     for b in np.nonzero(ok)[0]:
         assert relerr(res["x"][b], gen["x"][b]) <= 1e-11
