@@ -63,7 +63,7 @@ struct Ws {  // global workspace layout (doubles), per launch
   __host__ __device__ static size_t gpart(int nc) { return (size_t)nc * TT * GX; }
   static size_t bytes(int nc) {
     return 256 + sizeof(double) * (gpart(nc) + TT * GX + (size_t)nc * 4 * TT + (size_t)(R / 8) * 2 * 64 +
-                                   (size_t)R * TT + (size_t)R * 8);
+                                   (size_t)R * TT + (size_t)R * 8 + (size_t)R + (size_t)(R / 8) * 16);
   }
 };
 
@@ -85,7 +85,8 @@ struct GridSmem {
   int flags[8];
 };
 
-template <int R, int CW>
+// GEN: general variant only; !GEN: orthogonal / orthonormal (solver.py:382-395)
+template <int R, int CW, bool GEN>
 __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state st, const double* __restrict__ rows,
                                                      int64_t rstride, const double* __restrict__ tgts, int64_t tstride,
                                                      int64_t T, uint8_t* __restrict__ blog, double* __restrict__ clog,
@@ -104,6 +105,8 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
   double* ws_s = ws_r0 + (size_t)nc * 4 * TT;      // [IT][2][64]: S and G W partials
   double* ws_y = ws_s + (size_t)IT * 2 * 64;       // [R][TT]
   double* ws_w = ws_y + (size_t)R * TT;            // [R][8]
+  double* ws_z = ws_w + (size_t)R * 8;             // [R]: z = P gamma (non-general growth)
+  double* ws_d = ws_z + R;                         // [IT][16]: gamma.z, gamma^T W partials
   unsigned epoch = 0;
   unsigned nproj = 0;  // projections so far (selects the ws_r buffer)
 
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           break;
         }
         // ---- independent row tstar (solver.py:305-318, _grow solver.py:368-397)
-        {
+        if (GEN || cfg.variant == RGB_GENERAL) {
           const int ts = tstar;
           const double rinv = 1.0 / S.scal[ts];  // K = rej / |rej|^2 (one rounding more than a division)
           // C~[:r] -= gamma K^T, C~[r] = K on my columns; C[r] = a
@@ -438,6 +441,72 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             if (blog) blog[row] = 1;
             if (clog)
               for (int i = 0; i < R; ++i) clog[row * R + i] = (i == r) ? 1.0 : 0.0;
+          }
+          __syncthreads();
+          r += 1;
+        } else {
+          // orthogonal / orthonormal growth: C~[:r] and C[:r] stay, P gains an
+          // edge -alpha z and a corner alpha^2 (1 + gamma.z), z = P gamma
+          // (solver.py:307-310, 382-395); W gains alpha (y - a.x), a.x = a.x0 + gamma^T W
+          const int ts = tstar;
+          const double rsq = S.scal[ts];
+          if (owner) {
+            // z and the gamma.z / gamma^T W partials of my row block
+            if (tid < 8) {
+              const int i = 8 * c + tid;
+              double z = 0.0;
+              for (int i2 = 0; i2 < R; ++i2) z = fma(S.Ps[tid][i2], S.Gs[ts][i2], z);
+              ws_z[i] = z;
+              S.rd[tid] = z;
+            }
+            __syncthreads();
+            if (tid < 9) {
+              double v = 0.0;
+              for (int u = 0; u < 8; ++u)
+                v = fma(S.Gs[ts][8 * c + u], tid == 0 ? S.rd[u] : S.Wb[u][tid - 1], v);
+              ws_d[(size_t)c * 16 + tid] = v;
+            }
+          }
+          grid_sync(ctr, epoch);
+          const double resc = (cfg.variant == RGB_ORTHONORMAL) ? 1.0 / sqrt(rsq) : cfg.alpha;
+          const double last = 1.0 / resc;
+          const double alpha = 1.0 / last;
+          const double sc = alpha * rsq;
+          for (int e = tid; e < (CW / 4) * 4; e += NT) {  // C~[r] on my columns
+            const int kt = e >> 2, l = 4 * (r & 7) + (e & 3), jl = e;
+            const double rj = S.Rs[ts][jl];
+            S.Ds[r >> 3][kt][l] = (cfg.variant == RGB_ORTHONORMAL) ? alpha * rj : rj / sc;
+          }
+          for (int e = tid; e < CW; e += NT) {  // C[r] = alpha rej
+            const int kt = r >> 2, nt = e >> 3, l = 4 * (e & 7) + (r & 3);
+            S.Cs[kt][nt][l] = -(alpha * S.Rs[ts][e]);
+          }
+          if (owner) {
+            const bool rown = (r >> 3) == c;
+            double denom = 0.0;
+            if (rown) {
+              double dn = 0.0;
+              for (int u = 0; u < IT; ++u) dn += __ldcg(ws_d + (size_t)u * 16);
+              denom = 1.0 + dn;
+            }
+            for (int e = tid; e < 8 * R; e += NT) {
+              const int i = 8 * c + e / R, i2 = e % R;
+              double& P = S.Ps[e / R][i2];
+              if (i == r && i2 == r) P = alpha * alpha * denom;
+              else if (i2 == r) P = (i < r) ? -(alpha * S.rd[e / R]) : 0.0;
+              else if (i == r) P = (i2 < r) ? -(alpha * __ldcg(ws_z + i2)) : 0.0;
+            }
+            if (rown && tid < 8) {
+              double gw = 0.0;
+              for (int u = 0; u < IT; ++u) gw += __ldcg(ws_d + (size_t)u * 16 + 1 + tid);
+              S.Wb[r & 7][tid] = tid < k ? alpha * ((S.Yv[ts][tid] - S.Gs[ts][R + tid]) - gw) : 0.0;
+            }
+          }
+          if (c == 0 && tid == 0) {
+            const int64_t row = b * T + t0 + ts;
+            if (blog) blog[row] = 1;
+            if (clog)
+              for (int i = 0; i < R; ++i) clog[row * R + i] = i < r ? S.Gs[ts][i] : (i == r ? last : 0.0);
           }
           __syncthreads();
           r += 1;
@@ -486,7 +555,7 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
                          cudaStream_t stream, int num_sms) {
   const int nc = cfg.m / CW;
   if (nc > num_sms || nc < R / 8) return RGB_E_UNSUPPORTED;
-  auto kern = grd::grid_kernel<R, CW>;
+  auto kern = cfg.variant == RGB_GENERAL ? grd::grid_kernel<R, CW, true> : grd::grid_kernel<R, CW, false>;
   const size_t smem = sizeof(grd::GridSmem<R, CW>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return RGB_E_UNSUPPORTED;
@@ -512,7 +581,9 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
 }
 
 bool grid_supports(const rgb_config& cfg) {
-  if (cfg.dtype != RGB_F64 || cfg.variant != RGB_GENERAL || cfg.k < 1 || cfg.k > 8) return false;
+  const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
+                      (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
+  if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
   if (cfg.num_streams > 4) return false;  // a handful of large streams, one after the other
   return (cfg.m == 1024 && cfg.r_cap == 64) || (cfg.m == 2048 && cfg.r_cap == 512);
 }

@@ -473,6 +473,35 @@ def test_single_large_stream_grid_kernel(cfg, n):
     assert np.abs(D @ C.T - np.eye(r)).max() <= 1e-9
 
 
+@pytest.mark.parametrize("cfg,n", [("c2", 2048), ("c4", 1100)])
+@pytest.mark.parametrize("variant,alpha", [("orthogonal", 0.5), ("orthonormal", 1.0)])
+def test_single_large_stream_grid_kernel_variants(cfg, n, variant, alpha):
+    """Orthogonal / orthonormal factorisations on the grid kernel: branches,
+    rank and x against the oracle, the stored factors and the coords log;
+    the orthonormal basis is orthonormal (C C^T = I)."""
+    from paper_2106_11594_b200 import workloads
+
+    A, y = getattr(workloads, cfg)()
+    A, y = A[:n], y[:n]
+    rc = workloads.CONFIGS[cfg].r_cap
+    res = run_batched(A, y, r_cap=rc, variant=variant, alpha=alpha)
+    o = oracle.ingest(A[None], y[None], r_cap=rc, variant=variant, alpha=alpha, nthreads=1)
+    assert res["status"][0] == 0 and int(res["rank"][0]) == int(o["rank"][0]) == workloads.CONFIGS[cfg].r
+    assert np.array_equal(res["branch"][0], o["branch"][0])
+    assert relerr(res["x"][0, :, 0], oracle.solution(o)[0, :, 0]) <= 1e-10
+    bs = res["solver"]
+    r = int(res["rank"][0])
+    C = bs.basis_t[0, :r].cpu().numpy()
+    D = bs.dual_t[0, :r].cpu().numpy()
+    P = bs.gram_t[0, :r, :r].cpu().numpy()
+    assert relerr(C, o["C"][0, :r]) <= 1e-10
+    assert relerr(D, (o["C"] if variant == "orthonormal" else o["D"])[0, :r]) <= 1e-10
+    assert relerr(P, o["P"][0, :r, :r]) <= 1e-8
+    assert relerr(res["coords"][0], o["coords"][0]) <= 1e-9
+    if variant == "orthonormal":
+        assert np.abs(C @ C.T - np.eye(r)).max() <= 1e-9
+
+
 def _shape_rows(cfg, streams, n, rank_extra=0):
     """Rows of a config's shape; rank_extra > 0 appends independent rows so
     that the rank exceeds the device capacity."""
