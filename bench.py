@@ -48,13 +48,24 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c5", choices=sorted(workloads.CONFIGS))
-    ap.add_argument("--dtype", default="fp64", choices=["fp64", "fp32"])
+    # fp32: float32 rows/targets widened exactly into a float64 state (fp64
+    # arithmetic, fp64 parity; half the input bytes); fp32-state: float32 state
+    # and arithmetic (generic kernel, 1e-3 parity)
+    ap.add_argument("--dtype", default="fp64", choices=["fp64", "fp32", "fp32-state"])
+    ap.add_argument("--eps", type=float, default=None,
+                    help="fixed eps policy (EpsPolicy.fixed); default auto for fp64, 1e-5 for fp32 inputs")
     ap.add_argument("--streams", type=int, default=None, help="override B (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4096)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.eps is None and args.dtype == "fp32":
+        # float32 inputs carry ~6e-8 relative rounding: the auto policy's fp64
+        # threshold would read it as rank, so the fp32 workload runs with a
+        # fixed threshold above that noise (the reference's EpsPolicy.fixed)
+        args.eps = 1e-5
+    return args
 
 
 # -- algorithmic work --------------------------------------------
@@ -81,9 +92,11 @@ def algorithmic_flops(branch, m, k):
     return float(torch.where(dep, f_dep, f_ind).sum().item())
 
 
-def alg_bytes(S, n, m, k, s):
-    """Compulsory HBM bytes: rows + targets read, solutions written, 4 B of rank."""
-    return s * (S * n * (m + k) + S * m * k) + 4 * S
+def alg_bytes(S, n, m, k, s, sx=None):
+    """Compulsory HBM bytes: rows + targets read (s bytes per value), solutions
+    written (sx bytes per value, default s), 4 B of rank."""
+    sx = s if sx is None else sx
+    return s * S * n * (m + k) + sx * S * m * k + 4 * S
 
 
 # -- clocks ------------------------------------------------------------------------
@@ -200,12 +213,14 @@ def cpu_sample_inputs(cfg_name, count, rows_dev=None, tg_dev=None):
     return A[None], y[None, :, None]
 
 
-def cpu_baseline(cfg_name, dtype, rows, tg, reps=1):
+def cpu_baseline(cfg_name, dtype, rows, tg, reps=1, eps=None):
     from oracle import oracle
 
     cores = len(os.sched_getaffinity(0))
     cfg = workloads.CONFIGS[cfg_name]
-    npdt = np.float32 if dtype == "fp32" else np.float64
+    npdt = np.float32 if dtype == "fp32-state" else np.float64
+    if dtype != "fp64":  # float32 data (widened exactly for the fp64-state mode)
+        rows, tg = rows.astype(np.float32), tg.astype(np.float32)
     rows = rows.astype(npdt, copy=False)
     tg = tg.astype(npdt, copy=False)
     if rows.shape[0] == 1 and cfg.m * cfg.r > 100000:
@@ -217,7 +232,7 @@ def cpu_baseline(cfg_name, dtype, rows, tg, reps=1):
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        oracle.ingest(rows, tg, r_cap=cfg.r_cap, dtype=npdt,
+        oracle.ingest(rows, tg, r_cap=cfg.r_cap, dtype=npdt, eps=eps,
                       nthreads=cores, logs=False)
         dt = time.perf_counter() - t0
         best = dt if best is None else min(best, dt)
@@ -236,8 +251,8 @@ def run_reference(args):
     count = {"c5": 2048, "c3": 2048}.get(args.config, 1)
     rows, tg = cpu_sample_inputs(args.config, count)
     for _ in range(args.warmup):
-        cpu_baseline(args.config, args.dtype, rows[: min(64, len(rows))], tg[: min(64, len(rows))])
-    vals = [cpu_baseline(args.config, args.dtype, rows, tg) for _ in range(args.steps)]
+        cpu_baseline(args.config, args.dtype, rows[: min(64, len(rows))], tg[: min(64, len(rows))], eps=args.eps)
+    vals = [cpu_baseline(args.config, args.dtype, rows, tg, eps=args.eps) for _ in range(args.steps)]
     v = statistics.median([c["value"] for c in vals])
     cb = dict(vals[0])
     cb["value"] = v
@@ -246,7 +261,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_total / v,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64" if args.dtype == "fp64" else "f32", "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d))",
+        "dtype": "f32" if args.dtype == "fp32-state" else "f64", "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d))",
         "config": {"workload": args.config, "streams": cfg.streams, "n": cfg.n, "m": cfg.m, "k": cfg.k,
                    "rank": cfg.r, "sampled_streams": rows.shape[0]},
         "cpu_baseline": cb,
@@ -281,8 +296,9 @@ def run_ours(args):
     B = args.streams or cfg.streams
     b0, b1 = sharding.shard_range(B, world, rank)
     S = b1 - b0
-    tdtype = torch.float32 if args.dtype == "fp32" else torch.float64
-    esize = 4 if args.dtype == "fp32" else 8
+    tdtype = torch.float64 if args.dtype == "fp64" else torch.float32   # inputs
+    sdtype = torch.float32 if args.dtype == "fp32-state" else torch.float64  # state / arithmetic
+    esize = 4 if args.dtype != "fp64" else 8
 
     # inputs resident in HBM before timing (generation is not timed)
     if cfg.streams > 1:
@@ -292,7 +308,7 @@ def run_ours(args):
         rows = torch.as_tensor(A[None], dtype=tdtype, device=device)
         tg = torch.as_tensor(y[None, :, None], dtype=tdtype, device=device)
     n = rows.shape[1]
-    bs = BatchedSolver(S, cfg.m, k=cfg.k, r_cap=cfg.r_cap, dtype=tdtype, device=device)
+    bs = BatchedSolver(S, cfg.m, k=cfg.k, r_cap=cfg.r_cap, dtype=sdtype, eps=args.eps, device=device)
     stream = torch.cuda.current_stream(device)
 
     # one untimed pass with the branch log: exact algorithmic work + status census
@@ -365,7 +381,7 @@ def run_ours(args):
 
         ns = min(16, S)
         r_np, t_np = rows[:ns].cpu().numpy(), tg[:ns].cpu().numpy()
-        o = oracle.ingest(r_np.astype(np.float64), t_np.astype(np.float64), r_cap=cfg.r_cap,
+        o = oracle.ingest(r_np.astype(np.float64), t_np.astype(np.float64), r_cap=cfg.r_cap, eps=args.eps,
                           nthreads=8, logs=False)
         x = bs.solution[:ns].cpu().numpy()
         xo = oracle.solution(o)
@@ -373,7 +389,7 @@ def run_ours(args):
         errs = [float(np.abs(x[b] - xo[b]).max() / max(1.0, np.abs(xo[b]).max())) for b in range(ns) if ok[b]]
         parity = {"streams": ns, "rank_match": bool(np.array_equal(ranks[:ns][ok], o["rank"][ok])),
                   "x_relerr_max": max(errs) if errs else None,
-                  "tolerance": 1e-9 if args.dtype == "fp64" else 1e-3}
+                  "tolerance": 1e-3 if args.dtype == "fp32-state" else 1e-9}
         # streams the device froze at the rank capacity: the oracle, given room
         # to grow, must run away past the construction rank too (SURVEY.md
         # finding 0.3: the reference itself does on ~1 in 2048 C5 streams)
@@ -381,7 +397,7 @@ def run_ours(args):
         if len(capped):
             rc_ = torch.tensor(capped, device=device, dtype=torch.long)
             o2 = oracle.ingest(rows[rc_].cpu().numpy().astype(np.float64), tg[rc_].cpu().numpy().astype(np.float64),
-                               r_cap=n, nthreads=8, logs=False)
+                               r_cap=n, eps=args.eps, nthreads=8, logs=False)
             parity["rank_cap_streams_checked"] = int(len(capped))
             parity["rank_cap_oracle_ranks"] = [int(v) for v in o2["rank"]]
             parity["rank_cap_oracle_runaway"] = bool((o2["rank"] > cfg.r).all())
@@ -397,25 +413,28 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         count = {"c5": 2048, "c3": 2048}.get(args.config, 1)
         r_s, t_s = cpu_sample_inputs(args.config, min(count, S), rows, tg)
-        cpu = cpu_baseline(args.config, args.dtype, r_s, t_s)
+        cpu = cpu_baseline(args.config, args.dtype, r_s, t_s, eps=args.eps)
 
     if rank == 0:
         peaks = fp64_peak()
         mp = measured_peaks()
-        peak_tf = peaks.get("dmma") if args.dtype == "fp64" else None
+        peak_tf = peaks.get("dmma")
         peak_src = "live fp64 DMMA m8n8k4 probe (tools/fp64_peak.cu), this GPU, this run"
-        if args.dtype == "fp32":
+        if args.dtype == "fp32-state":
             peak_tf, peak_src = 2 * peaks.get("dfma", 0), "2x live fp64 DFMA probe (fp32 FMA rate)"
         achieved = flops_total / world / (kern_ms * 1e-3) / 1e12
-        byt = alg_bytes(S, n, cfg.m, cfg.k, esize)
+        byt = alg_bytes(S, n, cfg.m, cfg.k, esize, 4 if args.dtype == "fp32-state" else 8)
         hbm_gbs = byt / (kern_ms * 1e-3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.dtype == "fp64" else "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32-state" else "f64",
             "data": "synthetic: seeded A = G1 G2 per stream generated on device (SURVEY.md 8(d)); inputs resident in HBM",
             "config": {"workload": args.config, "streams": B, "n": n, "m": cfg.m, "rank": cfg.r, "k": cfg.k,
-                       "r_cap": cfg.r_cap, "variant": "general", "eps": "auto",
+                       "r_cap": cfg.r_cap, "variant": "general",
+                       "eps": "auto" if args.eps is None else f"fixed {args.eps:g}",
+                       "inputs": {"fp64": "fp64", "fp32": "fp32, widened exactly into the fp64 state on load",
+                                  "fp32-state": "fp32 (fp32 state and arithmetic)"}[args.dtype],
                        "l2": (f"inputs {in_bytes * world / 1e6:.0f} MB < 2x L2: L2 flushed (512 MB write) between "
                               "steps, outside the per-step events" if flush else
                               f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)"),
@@ -466,7 +485,7 @@ def run_e2e(args, bs, rows, tg, stream, world, local, device, esize):
     tg_h = torch.empty((S_e, n, k), dtype=tg.dtype, pin_memory=True)
     rows_h.copy_(rows[:S_e])
     tg_h.copy_(tg[:S_e])
-    x_h = torch.empty((S_e, k, m), dtype=rows.dtype, pin_memory=True)
+    x_h = torch.empty((S_e, k, m), dtype=bs.dtype, pin_memory=True)
     r_h = torch.empty(S_e, dtype=torch.int32, pin_memory=True)
     from paper_2106_11594_b200.batched import BatchedSolver
 
@@ -492,7 +511,7 @@ def run_e2e(args, bs, rows, tg, stream, world, local, device, esize):
     scale = S / S_e
     return {"_ms": ms * scale, "_steps": steps, "unit": UNIT,
             "h2d_bytes_per_step": int((rows_h.numel() + tg_h.numel()) * esize),
-            "d2h_bytes_per_step": int(x_h.numel() * esize + r_h.numel() * 4),
+            "d2h_bytes_per_step": int(x_h.numel() * x_h.element_size() + r_h.numel() * 4),
             "streams_measured": S_e, "chunk_streams": args.e2e_chunk,
             "note": "pinned host -> device copies overlapped with ingest; value scaled to the full batch"
                     if S_e != S else "pinned host -> device copies overlapped with ingest (BatchedSolver.ingest_host)"}

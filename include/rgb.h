@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define RGB_ABI_VERSION 1
+#define RGB_ABI_VERSION 2
 
 /* scalar kinds: scalars.py:141-147 (FLOAT64); FLOAT32 is a new kind */
 enum { RGB_F64 = 0, RGB_F32 = 1 };
@@ -109,6 +109,17 @@ int rgb_state_reset(const rgb_config *cfg, rgb_state *state, void *stream);
 int rgb_ingest(const rgb_config *cfg, rgb_state *state, const void *rows, int64_t rows_stride,
                const void *targets, int64_t targets_stride, int64_t T, const rgb_logs *logs,
                void *stream);
+
+/* rgb_ingest with single-precision rows and targets (same layout and strides,
+ * in float elements) folded into a state of cfg->dtype.  Every input value is
+ * widened exactly on load, so with an RGB_F64 state the result is identical to
+ * rgb_ingest on the widened inputs -- fp64 state and arithmetic, fp64 parity --
+ * while the input stream (HBM reads, host-link copies) halves.  With an RGB_F32
+ * state it is rgb_ingest.  No reference counterpart (the reference has no fp32
+ * kind, scalars.py:121); it serves the fp32 inputs of config 5. */
+int rgb_ingest_f32in(const rgb_config *cfg, rgb_state *state, const float *rows, int64_t rows_stride,
+                     const float *targets, int64_t targets_stride, int64_t T, const rgb_logs *logs,
+                     void *stream);
 
 /* RecursiveSolver.project + is_dependent (solver.py:210-229) for one row per
  * stream: coords [B][r_cap] (zero padded), rejection [B][m], rej_sq [B],

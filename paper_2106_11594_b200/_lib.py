@@ -14,14 +14,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RGB_LIB_PATH selects an alternative build of the same library (tuning A/B runs)
 LIB_PATH = os.environ.get("RGB_LIB_PATH") or os.path.join(HERE, "librgb.so")
 
-RGB_ABI_VERSION = 1
+RGB_ABI_VERSION = 2
 F64, F32 = 0, 1
 GENERAL, ORTHOGONAL, ORTHONORMAL = 0, 1, 2
 EPS_AUTO, EPS_FIXED = 0, 1
 OK, E_INVALID, E_UNSUPPORTED, E_CUDA = 0, -1, -2, -3
 ST_RANK_CAP, ST_NONFINITE, ST_BAD_ALPHA = 1, 2, 4
 
-EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest",
+EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest", "rgb_ingest_f32in",
            "rgb_project", "rgb_pinv", "rgb_covariance")
 
 
@@ -83,6 +83,7 @@ def load():
     lib.rgb_last_error.restype = ctypes.c_char_p
     lib.rgb_state_reset.argtypes = [cfgp, stp, vp]
     lib.rgb_ingest.argtypes = [cfgp, stp, vp, i64, vp, i64, i64, lgp, vp]
+    lib.rgb_ingest_f32in.argtypes = [cfgp, stp, vp, i64, vp, i64, i64, lgp, vp]
     lib.rgb_project.argtypes = [cfgp, stp, vp, vp, vp, vp, vp, vp]
     lib.rgb_pinv.argtypes = [cfgp, stp, vp, i64, vp, vp]
     lib.rgb_covariance.argtypes = [cfgp, stp, vp, vp]

@@ -112,6 +112,10 @@ class BatchedSolver:
                gain_out=None, stream=None):
         """Fold rows[B, T, m] / targets[B, T, k] (device tensors of this dtype).
 
+        A float64 solver also accepts float32 rows and targets: they are
+        widened exactly on load inside the kernel (rgb_ingest_f32in), so the
+        result equals ingesting rows.double() while reading half the bytes.
+
         Optional logs (preallocated device tensors): branch_log uint8 [B, T],
         coords_log [B, T, r_cap], resid_log [B, T, k], gain_out [B, m].
         Asynchronous on the current (or given) CUDA stream.
@@ -123,17 +127,28 @@ class BatchedSolver:
             targets = targets.unsqueeze(-1)
         if tuple(targets.shape) != (B, T, self.k):
             raise ValueError(f"targets have shape {tuple(targets.shape)}, expected ({B}, {T}, {self.k})")
+        f32in = self._f32_inputs(rows, targets)
         for t in (rows, targets):
-            if t.dtype != self.dtype or t.device != self.device:
+            if t.device != self.device:
                 raise ValueError("rows/targets must be device tensors of the solver dtype")
             if (t.shape[2] > 1 and t.stride(2) != 1) or (t.shape[1] > 1 and t.stride(1) != t.shape[2]):
                 raise ValueError("rows/targets must be contiguous within each stream")
         logs = _lib.Logs(_ptr(branch_log), _ptr(coords_log), _ptr(resid_log), _ptr(gain_out))
         cfg, st = self.config(), self.state()
         h = ctypes.c_void_p(stream.cuda_stream) if stream is not None else _stream_handle(self.device)
-        _lib.check(self.lib.rgb_ingest(ctypes.byref(cfg), ctypes.byref(st), _ptr(rows), rows.stride(0),
-                                       _ptr(targets), targets.stride(0), T, ctypes.byref(logs), h),
-                   "rgb_ingest")
+        fn = self.lib.rgb_ingest_f32in if f32in else self.lib.rgb_ingest
+        _lib.check(fn(ctypes.byref(cfg), ctypes.byref(st), _ptr(rows), rows.stride(0),
+                      _ptr(targets), targets.stride(0), T, ctypes.byref(logs), h), "rgb_ingest")
+
+    def _f32_inputs(self, rows, targets):
+        """True for float32 inputs into a float64 state; raises on any other mismatch."""
+        if rows.dtype != targets.dtype:
+            raise ValueError("rows and targets must have the same dtype")
+        if rows.dtype == self.dtype:
+            return False
+        if self.dtype == torch.float64 and rows.dtype == torch.float32:
+            return True
+        raise ValueError(f"rows/targets must be {self.dtype} (or float32 into a float64 solver), got {rows.dtype}")
 
     def ingest_host(self, rows_h, targets_h, *, chunk=4096):
         """Fold rows/targets that live in (pinned) HOST memory.
@@ -148,12 +163,15 @@ class BatchedSolver:
             targets_h = targets_h.unsqueeze(-1)
         if B != self.B or m != self.m or tuple(targets_h.shape) != (B, T, self.k):
             raise ValueError("host rows/targets do not match the solver shape")
+        f32in = self._f32_inputs(rows_h, targets_h)
+        in_dtype = rows_h.dtype
+        fn = self.lib.rgb_ingest_f32in if f32in else self.lib.rgb_ingest
         chunk = max(1, min(chunk, B))
         dev = self.device
         compute = torch.cuda.current_stream(dev)
         copy = torch.cuda.Stream(dev)
-        bufs = [(torch.empty((chunk, T, m), dtype=self.dtype, device=dev),
-                 torch.empty((chunk, T, self.k), dtype=self.dtype, device=dev)) for _ in range(2)]
+        bufs = [(torch.empty((chunk, T, m), dtype=in_dtype, device=dev),
+                 torch.empty((chunk, T, self.k), dtype=in_dtype, device=dev)) for _ in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
         for e in free:
@@ -171,9 +189,8 @@ class BatchedSolver:
             compute.wait_event(ready[i % 2])
             cfg, st = self.config(num_streams=n), self.state(s0)
             logs = _lib.Logs(None, None, None, None)
-            _lib.check(self.lib.rgb_ingest(ctypes.byref(cfg), ctypes.byref(st), _ptr(rb), rb.stride(0),
-                                           _ptr(tb), tb.stride(0), T, ctypes.byref(logs),
-                                           ctypes.c_void_p(compute.cuda_stream)), "rgb_ingest")
+            _lib.check(fn(ctypes.byref(cfg), ctypes.byref(st), _ptr(rb), rb.stride(0), _ptr(tb), tb.stride(0), T,
+                          ctypes.byref(logs), ctypes.c_void_p(compute.cuda_stream)), "rgb_ingest")
             free[i % 2].record(compute)
             launches += 1
         return launches

@@ -12,18 +12,19 @@
 namespace rgb {
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                   cudaStream_t stream, int num_sms);
+                   cudaStream_t stream, int num_sms, bool f32in);
 bool blocked_supports(const rgb_config& cfg);
 bool blocked_wg_supports(const rgb_config& cfg);
 bool grid_supports(const rgb_config& cfg);
 int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
-                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms);
+                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms,
+                bool f32in);
 int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                       const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                      cudaStream_t stream, int num_sms);
+                      cudaStream_t stream, int num_sms, bool f32in);
 int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                   cudaStream_t stream, int num_sms);
+                   cudaStream_t stream, int num_sms, bool f32in);
 int launch_project(const rgb_config& cfg, const rgb_state& st, const void* rows, void* coords,
                    void* rejection, void* rej_sq, uint8_t* dependent, cudaStream_t stream);
 int launch_pinv(const rgb_config& cfg, const rgb_state& st, const void* coords, int64_t n,
@@ -105,9 +106,9 @@ int rgb_state_reset(const rgb_config* cfg, rgb_state* st, void* stream) {
   return e == cudaSuccess ? RGB_OK : cuda_fail(e, "rgb_state_reset");
 }
 
-int rgb_ingest(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t rows_stride,
-               const void* targets, int64_t targets_stride, int64_t T, const rgb_logs* logs,
-               void* stream) {
+static int ingest_impl(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t rows_stride,
+                       const void* targets, int64_t targets_stride, int64_t T, const rgb_logs* logs,
+                       void* stream, bool f32in) {
   int rc = check_cfg(cfg);
   if (rc) return rc;
   if ((rc = check_state(cfg, st))) return rc;
@@ -125,18 +126,32 @@ int rgb_ingest(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t r
   rgb_state s2 = *st;
   if (cfg->variant == RGB_ORTHONORMAL) s2.dual = s2.basis;  // C~ is C (solver.py:168, 386)
   cudaStream_t s = (cudaStream_t)stream;
+  const int nsm = sm_count();
+  if (cfg->dtype == RGB_F32) f32in = false;  // the inputs already have the state's type
   rc = RGB_E_UNSUPPORTED;
   if (rgb::blocked_supports(*cfg) && !lg.resid && !lg.gain)
-    rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
+    rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::blocked_wg_supports(*cfg) && !lg.resid && !lg.gain)
-    rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
+    rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::grid_supports(*cfg) && !lg.resid && !lg.gain)
-    rc = rgb::launch_grid(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
+    rc = rgb::launch_grid(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   if (rc == RGB_E_UNSUPPORTED)
-    rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, sm_count());
+    rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   if (rc == RGB_E_UNSUPPORTED) return fail(rc, "shape beyond kernel limits (k <= 64, smem)");
   if (rc == RGB_E_CUDA) return cuda_fail(cudaGetLastError(), "rgb_ingest launch");
   return rc;
+}
+
+int rgb_ingest(const rgb_config* cfg, rgb_state* st, const void* rows, int64_t rows_stride,
+               const void* targets, int64_t targets_stride, int64_t T, const rgb_logs* logs,
+               void* stream) {
+  return ingest_impl(cfg, st, rows, rows_stride, targets, targets_stride, T, logs, stream, false);
+}
+
+int rgb_ingest_f32in(const rgb_config* cfg, rgb_state* st, const float* rows, int64_t rows_stride,
+                     const float* targets, int64_t targets_stride, int64_t T, const rgb_logs* logs,
+                     void* stream) {
+  return ingest_impl(cfg, st, rows, rows_stride, targets, targets_stride, T, logs, stream, true);
 }
 
 int rgb_project(const rgb_config* cfg, const rgb_state* st, const void* rows, void* coords,

@@ -47,11 +47,11 @@
 namespace rgb {
 namespace blk {
 
-template <int M, int R, int KC>
+template <int M, int R, int KC, typename TI>
 struct WarpSmem {
   double Cs[R / 4][M / 8][32];   // -C, the B operand of R = A + G (-C) accumulated onto A
-  double At[2][M / 8][32][2];    // double-buffered row tile, lane-slot layout
-  double Yt[2][32][2];           // targets y[t=2q+e][c=p]
+  TI At[2][M / 8][32][2];        // double-buffered row tile, lane-slot layout (input type)
+  TI Yt[2][32][2];               // targets y[t=2q+e][c=p]
   union {
     struct {
       double gam[R];             // coords of an independent row
@@ -69,17 +69,18 @@ struct WarpSmem {
 
 // GEN: general variant only (the headline instantiation); !GEN: orthogonal /
 // orthonormal, whose grow step differs (solver.py:382-395)
-template <int M, int R, int KC, int WARPS, bool GEN>
+// TI: input element type (double, or float widened exactly on load)
+template <int M, int R, int KC, int WARPS, bool GEN, typename TI>
 __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
-    rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
-    const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
+    rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
+    const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
     double* __restrict__ clog) {
   static_assert(M % 8 == 0 && R % 8 == 0 && KC == 8, "shape");
   constexpr int JT = M / 8, JK = M / 4, IT = R / 8, IK = R / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = lane >> 2, q = lane & 3;
-  WarpSmem<M, R, KC>& S = reinterpret_cast<WarpSmem<M, R, KC>*>(smem_raw)[wid];
+  WarpSmem<M, R, KC, TI>& S = reinterpret_cast<WarpSmem<M, R, KC, TI>*>(smem_raw)[wid];
   const int64_t nwarps = (int64_t)gridDim.x * WARPS;
 
   for (int64_t b = (int64_t)blockIdx.x * WARPS + wid; b < cfg.num_streams; b += nwarps) {
@@ -91,8 +92,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
     double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
     double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)KC * M;
-    const double* Rb = rows + b * rstride;
-    const double* Yb = tgts + b * tstride;
+    const TI* Rb = rows + b * rstride;
+    const TI* Yb = tgts + b * tstride;
 
     // ---- load the stream's state into fragment layouts -------------------------
     // A rank-0 stream is all zeros by the state contract (include/rgb.h: rows
@@ -149,14 +150,14 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         const int64_t t0 = tile * TT;
         const int64_t t = t0 + p;
         const bool ok = t < T;
-        const double* src = ok ? Rb + t * M : Rb;
+        const TI* src = ok ? Rb + t * M : Rb;
 #pragma unroll
-        for (int nt = 0; nt < JT; ++nt) cp_async16(&S.At[s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
+        for (int nt = 0; nt < JT; ++nt) cp_async_pair<TI>(&S.At[s][nt][lane][0], src + 8 * nt + 2 * q, ok);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t ty = t0 + 2 * q + e;
           const bool oky = ty < T;
-          cp_async8(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky ? 8 : 0);
+          cp_async_one<TI>(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky);
         }
       }
       cp_commit();
@@ -178,17 +179,17 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       double acc[JT][2];  // G C
     };
     auto front_begin = [&](int64_t tile, int s, Front& F, FrontAcc& X) {
-      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+      const TI* As = &S.At[s][0][lane][0];
       F.t0 = tile * TT;
       F.tv = (int)((T - F.t0) < TT ? (T - F.t0) : TT);
-      const double2 yy = *reinterpret_cast<const double2*>(&S.Yt[s][lane][0]);
+      const double2 yy = slot(&S.Yt[s][lane][0], 0);
       F.dyx[0] = yy.x;
       F.dyx[1] = yy.y;
       // row norms |a_t|^2 (solver.py:267)
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int nt = 0; nt < JT; ++nt) {
-        const double2 v = As[nt * 32];
+        const double2 v = slot(As, nt * 32);
         s4[(2 * nt) & 3] = fma(v.x, v.x, s4[(2 * nt) & 3]);
         s4[(2 * nt + 1) & 3] = fma(v.y, v.y, s4[(2 * nt + 1) & 3]);
       }
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       // R = A - G C accumulates onto the tile itself (C is stored negated)
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) {
-        const double2 v = As[jt * 32];
+        const double2 v = slot(As, jt * 32);
         X.acc[jt][0] = v.x;
         X.acc[jt][1] = v.y;
       }
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // G = A C~^T (M = t, N = i, K = j; solver.py:286): K steps 2J, 2J + 1
     // (hi = false: rank <= 8, rows 8.. of C~ are zero and N tile 1 is skipped)
     auto front_g1 = [&](int s, int J, Front& F, FrontAcc& X, bool hi = true) {
-      const double2 v = reinterpret_cast<const double2*>(&S.At[s][0][lane][0])[J * 32];
+      const double2 v = slot(&S.At[s][0][lane][0], J * 32);
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) {
         if (nt > 0 && !hi) break;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     };
     // |R_t|^2 = |a_t - (G C)_t|^2 and the rank test (solver.py:288-296)
     auto front_end = [&](int s, int row_start, Front& F, FrontAcc& X) {
-      const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+      const TI* As = &S.At[s][0][lane][0];
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) {
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
             *reinterpret_cast<double2*>(&S.u.ind.gam[8 * nt + 2 * q]) = make_double2(F.g[nt][0], F.g[nt][1]);
 #pragma unroll
           for (int jt = 0; jt < JT; ++jt) {
-            const double2 v = As[jt * 32];
+            const double2 v = slot(As, jt * 32);
             *reinterpret_cast<double2*>(&S.u.ind.kv[8 * jt + 2 * q]) =
                 make_double2(X.acc[jt][0] * rinv, X.acc[jt][1] * rinv);
             // the row itself (general: C[r] = a) or its rejection (other variants)
@@ -292,12 +293,12 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // a.x0 for a stream that did not start empty: Y0^T = x0^T A^T (M = c, N = t, K = j)
     auto front_x0 = [&](int s, Front& F) {
       if (has_x0) {
-        const double2* As = reinterpret_cast<const double2*>(&S.At[s][0][lane][0]);
+        const TI* As = &S.At[s][0][lane][0];
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int J = 0; J < JK / 2; ++J) {
           const double2 xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q));
-          const double2 v = As[J * 32];
+          const double2 v = slot(As, J * 32);
           mma(acc, xv.x, v.x);
           mma(acc, xv.y, v.y);
         }
@@ -600,13 +601,13 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // basis growth would cost 64 MMAs per row.  Leaves gamma, K = rej/|rej|^2
     // and the row in the scratch rows for grow_core(); returns |rej|^2, |a|^2.
     auto project_row = [&](int s, int ts, double& rsq_o, double& asq_o) {
-      const double2* Ar = reinterpret_cast<const double2*>(&S.At[s][0][4 * ts + q][0]);
+      const TI* Ar = &S.At[s][0][4 * ts + q][0];
       double gp[IT], a4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) gp[nt] = 0.0;
 #pragma unroll
       for (int J = 0; J < JK / 2; ++J) {  // my columns sigma(kt, q) = 8J + 2q + e
-        const double2 v = Ar[J * 32];
+        const double2 v = slot(Ar, J * 32);
         a4[(2 * J) & 3] = fma(v.x, v.x, a4[(2 * J) & 3]);
         a4[(2 * J + 1) & 3] = fma(v.y, v.y, a4[(2 * J + 1) & 3]);
 #pragma unroll
@@ -637,7 +638,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       for (int jt = 0; jt < JT; ++jt) {
         rp[jt] += __shfl_xor_sync(FULL, rp[jt], 1);
         rp[jt] += __shfl_xor_sync(FULL, rp[jt], 2);
-        rej[jt] = S.At[s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
+        rej[jt] = (double)S.At[s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
         r4[jt & 3] = fma(rej[jt], rej[jt], r4[jt & 3]);
       }
       double rsq = (r4[0] + r4[1]) + (r4[2] + r4[3]);
@@ -651,7 +652,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
           S.u.ind.kv[8 * jt + p] = rej[jt] * rinv;
-          S.u.ind.av[8 * jt + p] = GEN ? S.At[s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
+          S.u.ind.av[8 * jt + p] = GEN ? (double)S.At[s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
         }
       }
       __syncwarp();
@@ -677,7 +678,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           for (; ts < tv; ++ts) {
             double rsq, asq;
             project_row(s, ts, rsq, asq);
-            const double yv = S.Yt[s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p]
+            const double yv = (double)S.Yt[s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p]
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
             if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
             grow_core(yv, rsq, t0, ts);
@@ -813,13 +814,13 @@ bool blocked_supports(const rgb_config& cfg) {
   return cfg.dtype == RGB_F64 && var_ok && cfg.m == BM && cfg.r_cap == BR && cfg.k == BK;
 }
 
-int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
-                   const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                   cudaStream_t stream, int num_sms) {
-  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;  // per-row residuals: generic kernel
+template <typename TI>
+static int launch_blocked_t(const rgb_config& cfg, rgb_state& st, const TI* rows, int64_t rows_stride,
+                            const TI* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                            cudaStream_t stream, int num_sms) {
   const bool gen = cfg.variant == RGB_GENERAL;
-  auto kern = gen ? blk::blocked_kernel<BM, BR, BK, BWARPS, true> : blk::blocked_kernel<BM, BR, BK, BWARPS, false>;
-  const size_t smem = sizeof(blk::WarpSmem<BM, BR, BK>) * BWARPS;
+  auto kern = gen ? blk::blocked_kernel<BM, BR, BK, BWARPS, true, TI> : blk::blocked_kernel<BM, BR, BK, BWARPS, false, TI>;
+  const size_t smem = sizeof(blk::WarpSmem<BM, BR, BK, TI>) * BWARPS;
   static bool attr[2] = {false, false};
   if (!attr[gen]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -831,10 +832,20 @@ int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64
   int64_t need = (cfg.num_streams + BWARPS - 1) / BWARPS;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > need) grid = need;
-  kern<<<(unsigned)grid, BWARPS * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                      (const double*)targets, tg_stride, T, logs.branch,
-                                                      (double*)logs.coords);
+  kern<<<(unsigned)grid, BWARPS * 32, smem, stream>>>(cfg, st, rows, rows_stride, targets, tg_stride, T,
+                                                      logs.branch, (double*)logs.coords);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                   const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                   cudaStream_t stream, int num_sms, bool f32in) {
+  if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;  // per-row residuals: generic kernel
+  if (f32in)
+    return launch_blocked_t(cfg, st, (const float*)rows, rows_stride, (const float*)targets, tg_stride, T, logs,
+                            stream, num_sms);
+  return launch_blocked_t(cfg, st, (const double*)rows, rows_stride, (const double*)targets, tg_stride, T, logs,
+                          stream, num_sms);
 }
 
 }  // namespace rgb

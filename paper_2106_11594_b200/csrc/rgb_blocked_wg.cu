@@ -22,12 +22,12 @@
 namespace rgb {
 namespace blk {
 
-template <int R, int WG>
+template <int R, int WG, typename TI>
 struct GroupSmem {
   static constexpr int M = 32 * WG, IT = R / 8, IK = R / 4;
   double Cs[WG][IK][4][32];          // -C, per warp column slice
-  double At[WG][2][4][32][2];        // row tiles, per warp column slice, 2 stages
-  double Yt[WG][2][32][2];           // targets y[t=2q+e][c=p], per warp copy
+  TI At[WG][2][4][32][2];        // row tiles, per warp column slice, 2 stages
+  TI Yt[WG][2][32][2];           // targets y[t=2q+e][c=p], per warp copy
   double Gp[WG][IT][32][2];          // partial G of each warp
   double red[3][WG][32][2];          // asq / rsq / dyx partials
   double Sp[WG][32][2];              // partial S (and G W)
@@ -38,15 +38,15 @@ struct GroupSmem {
 };
 
 // GEN: general variant only; !GEN: orthogonal / orthonormal (solver.py:382-395)
-template <int R, int WG, bool GEN>
+template <int R, int WG, bool GEN, typename TI>
 __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
-    rgb_config cfg, rgb_state st, const double* __restrict__ rows, int64_t rstride,
-    const double* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
+    rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
+    const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
     double* __restrict__ clog) {
-  constexpr int M = 32 * WG, IT = R / 8, IK = R / 4, KC = 8;
+  constexpr int M = 32 * WG, IT = R / 8, IK = R / 4;
   static_assert(R % 8 == 0 && R <= 32 && IT <= WG, "shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GroupSmem<R, WG>& S = *reinterpret_cast<GroupSmem<R, WG>*>(smem_raw);
+  GroupSmem<R, WG, TI>& S = *reinterpret_cast<GroupSmem<R, WG, TI>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int p = lane >> 2, q = lane & 3;
   const int k = cfg.k;
@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
     double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
     double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
-    const double* Rb = rows + b * rstride;
-    const double* Yb = tgts + b * tstride;
+    const TI* Rb = rows + b * rstride;
+    const TI* Yb = tgts + b * tstride;
 
     // ---- state (rank 0 is all zeros by the state contract) ------------------------
     const bool fresh = (r == 0);
@@ -103,14 +103,14 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         const int64_t t0 = tile * TT;
         const int64_t t = t0 + p;
         const bool ok = t < T;
-        const double* src = ok ? Rb + t * M + j0 : Rb;
+        const TI* src = ok ? Rb + t * M + j0 : Rb;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) cp_async16(&S.At[w][s][nt][lane][0], src + 8 * nt + 2 * q, ok ? 16 : 0);
+        for (int nt = 0; nt < 4; ++nt) cp_async_pair<TI>(&S.At[w][s][nt][lane][0], src + 8 * nt + 2 * q, ok);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t ty = t0 + 2 * q + e;
           const bool oky = ty < T && p < k;
-          cp_async8(&S.Yt[w][s][lane][e], oky ? Yb + ty * k + p : Yb, oky ? 8 : 0);
+          cp_async_one<TI>(&S.Yt[w][s][lane][e], oky ? Yb + ty * k + p : Yb, oky);
         }
       }
       cp_commit();
@@ -128,10 +128,10 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 
     // projection of one tile and the rank test (solver.py:286-296)
     auto front = [&](int64_t tile, int s, int row_start, Front& F) {
-      const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
+      const TI* As = &S.At[w][s][0][lane][0];
       F.t0 = tile * TT;
       F.tv = (int)((T - F.t0) < TT ? (T - F.t0) : TT);
-      const double2 yy = *reinterpret_cast<const double2*>(&S.Yt[w][s][lane][0]);
+      const double2 yy = slot(&S.Yt[w][s][lane][0], 0);
       const int nti = (r + 7) >> 3;  // N tiles of G that can be nonzero
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
       double g[IT][2], g2[IT][2];
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = g2[nt][0] = g2[nt][1] = 0.0;
 #pragma unroll
       for (int J = 0; J < 4; ++J) {
-        const double2 v = As[J * 32];
+        const double2 v = slot(As, J * 32);
         s4[(2 * J) & 3] = fma(v.x, v.x, s4[(2 * J) & 3]);
         s4[(2 * J + 1) & 3] = fma(v.y, v.y, s4[(2 * J + 1) & 3]);
 #pragma unroll
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         for (int J = 0; J < 4; ++J) {
           double2 xv = make_double2(0.0, 0.0);
           if (p < k) xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + j0 + 8 * J + 2 * q));
-          const double2 v = As[J * 32];
+          const double2 v = slot(As, J * 32);
           mma(y0, xv.x, v.x);
           mma(y0, xv.y, v.y);
         }
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       // R = A - G C on the own columns (C stored negated, accumulated onto A)
 #pragma unroll
       for (int jt = 0; jt < 4; ++jt) {
-        const double2 v = As[jt * 32];
+        const double2 v = slot(As, jt * 32);
         F.acc[jt][0] = v.x;
         F.acc[jt][1] = v.y;
       }
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     // independent row ts (solver.py:305-318, _grow solver.py:368-397)
     auto grow = [&](const Front& F, int s, int ts) {
       if (p == ts) {
-        const double2* As = reinterpret_cast<const double2*>(&S.At[w][s][0][lane][0]);
+        const TI* As = &S.At[w][s][0][lane][0];
         const double rinv = 1.0 / F.rsq;  // K = rej / |rej|^2, one rounding more than a division
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt) {
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
               make_double2(F.acc[jt][0] * rinv, F.acc[jt][1] * rinv);
           // the row itself (general: C[r] = a) or its rejection (other variants)
           *reinterpret_cast<double2*>(&S.av[j0 + 8 * jt + 2 * q]) =
-              GEN ? As[jt * 32] : make_double2(F.acc[jt][0], F.acc[jt][1]);
+              GEN ? slot(As, jt * 32) : make_double2(F.acc[jt][0], F.acc[jt][1]);
         }
         if (w == 0) {
 #pragma unroll
@@ -491,13 +491,13 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     // (re-projecting the whole tile after each growth costs 64 MMAs per warp).
     // Leaves gamma, K and the row in the scratch rows; returns |rej|^2, |a|^2.
     auto project_row = [&](int s, int ts, double& rsq_o, double& asq_o) {
-      const double2* Ar = reinterpret_cast<const double2*>(&S.At[w][s][0][4 * ts + q][0]);
+      const TI* Ar = &S.At[w][s][0][4 * ts + q][0];
       double gp[IT], a2 = 0.0;
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) gp[nt] = 0.0;
 #pragma unroll
       for (int J = 0; J < 4; ++J) {  // my columns j0 + sigma(kt, q) = j0 + 8J + 2q + e
-        const double2 v = Ar[J * 32];
+        const double2 v = slot(Ar, J * 32);
         a2 = fma(v.x, v.x, fma(v.y, v.y, a2));
 #pragma unroll
         for (int nt = 0; nt < IT; ++nt) gp[nt] = fma(Dt[nt][2 * J], v.x, fma(Dt[nt][2 * J + 1], v.y, gp[nt]));
@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       for (int jt = 0; jt < 4; ++jt) {
         rp[jt] += __shfl_xor_sync(FULL, rp[jt], 1);
         rp[jt] += __shfl_xor_sync(FULL, rp[jt], 2);
-        rej[jt] = S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
+        rej[jt] = (double)S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] + rp[jt];
         r2 = fma(rej[jt], rej[jt], r2);
       }
       r2 += __shfl_xor_sync(FULL, r2, 4);
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt) {
           S.kv[j0 + 8 * jt + p] = rej[jt] * rinv;
-          S.av[j0 + 8 * jt + p] = GEN ? S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
+          S.av[j0 + 8 * jt + p] = GEN ? (double)S.At[w][s][jt][4 * ts + (p >> 1)][p & 1] : rej[jt];
         }
         if (w == 0) {
 #pragma unroll
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
           for (; ts < tv; ++ts) {
             double rsq, asq;
             project_row(s, ts, rsq, asq);
-            const double yv = S.Yt[w][s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p] (0 for c >= k)
+            const double yv = (double)S.Yt[w][s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p] (0 for c >= k)
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
             if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
             grow_core(yv, rsq, t0, ts);
@@ -697,13 +697,13 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 
 // Instantiations: (r_cap, warps) with m = 32 * warps -- config 3 (m 128,
 // r_cap 32) and config 1 (m 256, r_cap 16, one stream: 8 warps share its work).
-template <int R, int WG>
+template <int R, int WG, typename TI>
 static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                      cudaStream_t stream, int num_sms) {
   const bool gen = cfg.variant == RGB_GENERAL;
-  auto kern = gen ? blk::blocked_wg_kernel<R, WG, true> : blk::blocked_wg_kernel<R, WG, false>;
-  const size_t smem = sizeof(blk::GroupSmem<R, WG>);
+  auto kern = gen ? blk::blocked_wg_kernel<R, WG, true, TI> : blk::blocked_wg_kernel<R, WG, false, TI>;
+  const size_t smem = sizeof(blk::GroupSmem<R, WG, TI>);
   static bool attr[2] = {false, false};
   if (!attr[gen]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -714,9 +714,8 @@ static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > cfg.num_streams) grid = cfg.num_streams;
-  kern<<<(unsigned)grid, WG * 32, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                  (const double*)targets, tg_stride, T, logs.branch,
-                                                  (double*)logs.coords);
+  kern<<<(unsigned)grid, WG * 32, smem, stream>>>(cfg, st, (const TI*)rows, rows_stride, (const TI*)targets,
+                                                  tg_stride, T, logs.branch, (double*)logs.coords);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
@@ -729,12 +728,14 @@ bool blocked_wg_supports(const rgb_config& cfg) {
 
 int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                       const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                      cudaStream_t stream, int num_sms) {
+                      cudaStream_t stream, int num_sms, bool f32in) {
   if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
   if (cfg.m == 128 && cfg.r_cap == 32)
-    return launch_wg<32, 4>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    return f32in ? launch_wg<32, 4, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_wg<32, 4, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   if (cfg.m == 256 && cfg.r_cap == 16)
-    return launch_wg<16, 8>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    return f32in ? launch_wg<16, 8, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_wg<16, 8, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   return RGB_E_UNSUPPORTED;
 }
 

@@ -42,10 +42,11 @@ __device__ __forceinline__ void block_reduce(int nv, REAL* red, REAL* out, F par
   __syncthreads();
 }
 
-template <typename REAL>
+// TI: input element type (REAL, or float widened exactly into a double state)
+template <typename REAL, typename TI>
 __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
-    rgb_config cfg, rgb_state st, const REAL* __restrict__ rows, int64_t rows_stride,
-    const REAL* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs) {
+    rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rows_stride,
+    const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
   REAL* a_s = reinterpret_cast<REAL*>(smem_raw);        // m
@@ -64,16 +65,16 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
     REAL* D = (var == RGB_ORTHONORMAL) ? C : reinterpret_cast<REAL*>(st.dual) + b * (int64_t)rc * m;
     REAL* P = reinterpret_cast<REAL*>(st.gram_inv) + b * (int64_t)rc * rc;
     REAL* X = reinterpret_cast<REAL*>(st.x) + b * (int64_t)k * m;
-    const REAL* R = rows + b * rows_stride;
-    const REAL* Y = targets + b * tg_stride;
+    const TI* R = rows + b * rows_stride;
+    const TI* Y = targets + b * tg_stride;
     int r = st.rank[b];
     int status = st.status[b];
     int64_t nobs = st.nobs[b];
     if (status) continue;
     for (int64_t t = 0; t < T; ++t) {
-      const REAL* a = R + t * m;
-      for (int j = tid; j < m; j += GEN_NT) a_s[j] = a[j];
-      for (int c = tid; c < k; c += GEN_NT) y_s[c] = Y[t * k + c];
+      const TI* a = R + t * m;
+      for (int j = tid; j < m; j += GEN_NT) a_s[j] = (REAL)a[j];
+      for (int c = tid; c < k; c += GEN_NT) y_s[c] = (REAL)Y[t * k + c];
       __syncthreads();
       // coords = C~ a (solver.py:286): warp per dual row, lanes over columns
       for (int i = w; i < r; i += GEN_NW) {
@@ -222,19 +223,24 @@ size_t generic_smem_bytes(const rgb_config& cfg) {
 
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                   cudaStream_t stream, int num_sms) {
+                   cudaStream_t stream, int num_sms, bool f32in) {
   if (cfg.k > GEN_MAX_K) return RGB_E_UNSUPPORTED;
   size_t smem = generic_smem_bytes(cfg);
   if (smem > 200 * 1024) return RGB_E_UNSUPPORTED;
   int64_t grid = cfg.num_streams < (int64_t)num_sms * 8 ? cfg.num_streams : (int64_t)num_sms * 8;
   if (grid < 1) return RGB_OK;
-  if (cfg.dtype == RGB_F64) {
-    auto kern = generic_ingest_kernel<double>;
+  if (cfg.dtype == RGB_F64 && f32in) {
+    auto kern = generic_ingest_kernel<double, float>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
+                                                   (const float*)targets, tg_stride, T, logs);
+  } else if (cfg.dtype == RGB_F64) {
+    auto kern = generic_ingest_kernel<double, double>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
                                                    (const double*)targets, tg_stride, T, logs);
   } else {
-    auto kern = generic_ingest_kernel<float>;
+    auto kern = generic_ingest_kernel<float, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
                                                   (const float*)targets, tg_stride, T, logs);

@@ -86,9 +86,9 @@ struct GridSmem {
 };
 
 // GEN: general variant only; !GEN: orthogonal / orthonormal (solver.py:382-395)
-template <int R, int CW, bool GEN>
-__global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state st, const double* __restrict__ rows,
-                                                     int64_t rstride, const double* __restrict__ tgts, int64_t tstride,
+template <int R, int CW, bool GEN, typename TI>
+__global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state st, const TI* __restrict__ rows,
+                                                     int64_t rstride, const TI* __restrict__ tgts, int64_t tstride,
                                                      int64_t T, uint8_t* __restrict__ blog, double* __restrict__ clog,
                                                      double* __restrict__ ws, unsigned* __restrict__ ctr) {
   constexpr int IT = R / 8, GX = R + 8, NXT = (R + 8) / 8;
@@ -119,8 +119,8 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
     double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
     double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
-    const double* Rb = rows + b * rstride;
-    const double* Yb = tgts + b * tstride;
+    const TI* Rb = rows + b * rstride;
+    const TI* Yb = tgts + b * tstride;
 
     // ---- load my slices: C~ (+ x0^T as rows R..R+7), -C, my P / W blocks ---------
     for (int e = tid; e < NXT * (CW / 4) * 32; e += NT) {
@@ -150,11 +150,11 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       // tile rows of my columns and the targets
       for (int e = tid; e < TT * CW; e += NT) {
         const int t = e / CW, j = e % CW;
-        S.At[t][j] = t < tv ? Rb[(t0 + t) * M + c0 + j] : 0.0;
+        S.At[t][j] = t < tv ? (double)Rb[(t0 + t) * M + c0 + j] : 0.0;
       }
       for (int e = tid; e < 64; e += NT) {
         const int t = e >> 3, cc = e & 7;
-        S.Yv[t][cc] = (t < tv && cc < k) ? Yb[(t0 + t) * k + cc] : 0.0;
+        S.Yv[t][cc] = (t < tv && cc < k) ? (double)Yb[(t0 + t) * k + cc] : 0.0;
       }
       __syncthreads();
       int row_start = 0;
@@ -549,13 +549,13 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
 
 }  // namespace grd
 
-template <int R, int CW>
+template <int R, int CW, typename TI>
 static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                          const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                          cudaStream_t stream, int num_sms) {
   const int nc = cfg.m / CW;
   if (nc > num_sms || nc < R / 8) return RGB_E_UNSUPPORTED;
-  auto kern = cfg.variant == RGB_GENERAL ? grd::grid_kernel<R, CW, true> : grd::grid_kernel<R, CW, false>;
+  auto kern = cfg.variant == RGB_GENERAL ? grd::grid_kernel<R, CW, true, TI> : grd::grid_kernel<R, CW, false, TI>;
   const size_t smem = sizeof(grd::GridSmem<R, CW>);
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return RGB_E_UNSUPPORTED;
@@ -568,8 +568,8 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
   cudaMemsetAsync(ws, 0, 256, stream);
   double* wsd = reinterpret_cast<double*>(ws);
   unsigned* ctr = reinterpret_cast<unsigned*>(ws);
-  const double* rp = (const double*)rows;
-  const double* tp = (const double*)targets;
+  const TI* rp = (const TI*)rows;
+  const TI* tp = (const TI*)targets;
   uint8_t* bl = logs.branch;
   double* cl = (double*)logs.coords;
   rgb_config c2 = cfg;
@@ -589,12 +589,14 @@ bool grid_supports(const rgb_config& cfg) {
 }
 
 int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
-                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms) {
+                int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms, bool f32in) {
   if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
   if (cfg.m == 1024 && cfg.r_cap == 64)
-    return launch_grid_t<64, 8>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    return f32in ? launch_grid_t<64, 8, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_grid_t<64, 8, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   if (cfg.m == 2048 && cfg.r_cap == 512)
-    return launch_grid_t<512, 16>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    return f32in ? launch_grid_t<512, 16, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_grid_t<512, 16, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   return RGB_E_UNSUPPORTED;
 }
 

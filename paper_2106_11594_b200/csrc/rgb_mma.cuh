@@ -33,6 +33,28 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int byte
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+// one lane slot of the staged input: 2 consecutive values (fp64 or fp32 input),
+// widened exactly to double
+template <typename TI>
+__device__ __forceinline__ void cp_async_pair(TI* smem, const TI* gmem, bool ok) {
+  if constexpr (sizeof(TI) == 8) cp_async16(smem, gmem, ok ? 16 : 0);
+  else cp_async8(smem, gmem, ok ? 8 : 0);
+}
+template <typename TI>
+__device__ __forceinline__ void cp_async_one(TI* smem, const TI* gmem, bool ok) {
+  if constexpr (sizeof(TI) == 8) cp_async8(smem, gmem, ok ? 8 : 0);
+  else cp_async4(smem, gmem, ok ? 4 : 0);
+}
+// lane slot i (a pair of values) of a staged tile, widened to double
+__device__ __forceinline__ double2 slot(const double* base, int i) { return reinterpret_cast<const double2*>(base)[i]; }
+__device__ __forceinline__ double2 slot(const float* base, int i) {
+  const float2 f = reinterpret_cast<const float2*>(base)[i];
+  return make_double2((double)f.x, (double)f.y);
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }

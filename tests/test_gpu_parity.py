@@ -604,3 +604,37 @@ def test_variants_on_tensor_core_kernel(cfg, r_cap, n, variant, alpha):
     for b in np.nonzero(ok)[0][:4]:
         ob = {key: v[b:b + 1] for key, v in o.items() if isinstance(v, np.ndarray)}
         assert relerr(pinv[b], oracle.pinv_closed_form(ob, variant=variant)) <= 1e-9
+
+
+@pytest.mark.parametrize("cfg,r_cap,streams,n", [("c5", 16, 24, 512), ("c3", 32, 12, 256), ("c2", 64, 1, 512),
+                                                 ("odd", 8, 5, 96)])
+def test_fp32_inputs_into_fp64_state_equal_widened_fp64(cfg, r_cap, streams, n):
+    """rgb_ingest_f32in (float32 rows/targets, float64 state) is the fp64 path
+    on the widened inputs, on every kernel (one-warp, warp-group, grid,
+    generic): identical branches, ranks, x and factors, bit for bit."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    if cfg == "odd":
+        rng = np.random.default_rng(3)
+        rows = (rng.standard_normal((streams, n, 6)) @ rng.standard_normal((6, 40)))
+        tg = rng.standard_normal((streams, n, 3))
+    else:
+        rows, tg = _shape_rows(cfg, list(range(streams)), n)
+    rows32 = torch.as_tensor(rows, dtype=torch.float32)
+    tg32 = torch.as_tensor(tg.reshape(rows.shape[0], n, -1), dtype=torch.float32)
+    B, T, m = rows32.shape
+    k = tg32.shape[2]
+    out = []
+    for inp in ((rows32.cuda(), tg32.cuda()), (rows32.double().cuda(), tg32.double().cuda())):
+        bs = BatchedSolver(B, m, k=k, r_cap=r_cap)
+        br = torch.zeros((B, T), dtype=torch.uint8, device="cuda")
+        bs.ingest(*inp, branch_log=br)
+        torch.cuda.synchronize()
+        out.append((br.cpu(), bs.rank.cpu(), bs.solution.cpu(), bs.basis_t.cpu(), bs.dual_t.cpu(), bs.gram_t.cpu()))
+    for a, b in zip(*out):
+        assert torch.equal(a, b)
+    # and the chunked host pipeline with float32 pinned buffers
+    bs = BatchedSolver(B, m, k=k, r_cap=r_cap)
+    bs.ingest_host(rows32.pin_memory(), tg32.pin_memory(), chunk=max(1, B // 2))
+    torch.cuda.synchronize()
+    assert torch.equal(bs.solution.cpu(), out[1][2])
