@@ -16,6 +16,10 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
 bool blocked_supports(const rgb_config& cfg);
 bool blocked_wg_supports(const rgb_config& cfg);
 bool grid_supports(const rgb_config& cfg);
+bool cluster_supports(const rgb_config& cfg);
+int launch_cluster(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
+                   int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms,
+                   bool f32in);
 int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
                 int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms,
                 bool f32in);
@@ -133,7 +137,9 @@ static int ingest_impl(const rgb_config* cfg, rgb_state* st, const void* rows, i
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::blocked_wg_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
-  else if (rgb::grid_supports(*cfg) && !lg.resid && !lg.gain)
+  else if (rgb::cluster_supports(*cfg) && !lg.resid && !lg.gain)
+    rc = rgb::launch_cluster(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
+  if (rc == RGB_E_UNSUPPORTED && rgb::grid_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_grid(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   if (rc == RGB_E_UNSUPPORTED)
     rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);

@@ -638,3 +638,70 @@ def test_fp32_inputs_into_fp64_state_equal_widened_fp64(cfg, r_cap, streams, n):
     bs.ingest_host(rows32.pin_memory(), tg32.pin_memory(), chunk=max(1, B // 2))
     torch.cuda.synchronize()
     assert torch.equal(bs.solution.cpu(), out[1][2])
+
+
+def _lowrank_streams(B, n, m, r, k, seed):
+    rng = np.random.default_rng(seed)
+    rows = np.einsum("bnr,brm->bnm", rng.standard_normal((B, n, r)), rng.standard_normal((B, r, m)))
+    return np.ascontiguousarray(rows), rng.standard_normal((B, n, k))
+
+
+@pytest.mark.parametrize("m,B,r,k", [(128, 5, 40, 1), (512, 3, 64, 3), (1024, 2, 50, 8)])
+@pytest.mark.parametrize("variant", ["general", "orthonormal"])
+def test_cluster_kernel_shapes_against_oracle(m, B, r, k, variant):
+    """The thread-block-cluster kernel (r_cap 64, m = 64 x cluster size, 32-row
+    panels) on several cluster sizes and several streams per launch (one
+    cluster each), with a row count that leaves a partial last panel, and as
+    two continuation calls: branches, ranks, x and the factors against the
+    oracle."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    n = 301
+    rows, tg = _lowrank_streams(B, n, m, r, k, seed=m + B)
+    o = oracle.ingest(rows, tg, r_cap=64, variant=variant, nthreads=8)
+    assert (o["rank"] == r).all() and (o["status"] == 0).all()
+    for split in (None, 77):
+        bs = BatchedSolver(B, m, k=k, r_cap=64, variant=variant)
+        br = torch.zeros((B, n), dtype=torch.uint8, device="cuda")
+        if split is None:
+            bs.ingest(dev(rows), dev(tg), branch_log=br)
+        else:
+            br1 = torch.zeros((B, split), dtype=torch.uint8, device="cuda")  # logs are [B][T] contiguous
+            bs.ingest(dev(rows[:, :split]), dev(tg[:, :split]), branch_log=br1)
+            br2 = torch.zeros((B, n - split), dtype=torch.uint8, device="cuda")
+            bs.ingest(dev(rows[:, split:]), dev(tg[:, split:]), branch_log=br2)
+            br = torch.cat([br1, br2], dim=1)
+        torch.cuda.synchronize()
+        assert np.array_equal(bs.rank.cpu().numpy(), o["rank"])
+        assert np.array_equal(br.cpu().numpy(), o["branch"])
+        assert (bs.nobs_t.cpu().numpy() == n).all() and (bs.status.cpu().numpy() == 0).all()
+        X = bs.solution.cpu().numpy()
+        XO = oracle.solution(o)
+        for b in range(B):
+            assert relerr(X[b], XO[b]) <= 1e-10
+        C = bs.basis_t.cpu().numpy()
+        P = bs.gram_t.cpu().numpy()
+        assert relerr(C, o["C"]) <= 1e-10
+        assert relerr(P, o["P"]) <= 1e-8
+
+
+def test_cluster_kernel_nonfinite_and_rank_cap():
+    """A NaN row freezes its stream at that row (RGB_ST_NONFINITE, nobs = the
+    rows before it); a stream whose rank would pass 64 freezes with
+    RGB_ST_RANK_CAP; the other streams of the launch are unaffected."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    B, n, m = 3, 200, 256
+    rows, tg = _lowrank_streams(B, n, m, 20, 1, seed=9)
+    rows[1, 70, 5] = np.nan
+    rows[2, 100:150] = np.random.default_rng(2).standard_normal((50, m))  # rank 20 + 50 > 64
+    bs = BatchedSolver(B, m, k=1, r_cap=64)
+    bs.ingest(dev(rows), dev(tg))
+    torch.cuda.synchronize()
+    st = bs.status.cpu().numpy()
+    nobs = bs.nobs_t.cpu().numpy()
+    assert st[0] == 0 and nobs[0] == n
+    assert st[1] & 2 and nobs[1] == 70
+    assert st[2] & 1 and bs.rank.cpu().numpy()[2] == 64
+    o = oracle.ingest(rows[:1], tg[:1], r_cap=64, nthreads=1)
+    assert relerr(bs.solution.cpu().numpy()[0], oracle.solution(o)[0]) <= 1e-10
