@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
     int status = st.status[b];
     if (status) continue;  // uniform across the block
     int r = st.rank[b];
+    double esq = eps_sq<double>(cfg, r);  // rank-test threshold, refreshed when r grows
     const int64_t nobs0 = st.nobs[b];
     double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       const unsigned yb1 = __ballot_sync(FULL, !isfinite(F.dyx[1]));
       const bool ybad = (((p & 1) ? yb1 : yb0) & (0x11111111u << (p >> 1))) != 0u;
       const bool valid = p >= row_start && p < F.tv;
-      const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
+      const bool dep = is_dependent<double>(rsq, asq, esq);
       const bool bad = !isfinite(asq) || ybad;
       const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
       F.badm = __ballot_sync(FULL, q == 0 && valid && bad);
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       }
       __syncthreads();
       r += 1;
+      esq = eps_sq<double>(cfg, r);
     };
     // independent row ts (solver.py:305-318, _grow solver.py:368-397)
     auto grow = [&](const Front& F, int s, int ts) {
@@ -590,7 +592,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
             project_row(s, ts, rsq, asq);
             const double yv = (double)S.Yt[w][s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p] (0 for c >= k)
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
-            if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
+            if (bad || r >= R || is_dependent<double>(rsq, asq, esq)) break;
             grow_core(yv, rsq, t0, ts);
           }
           if (ts < tv) {
