@@ -65,6 +65,29 @@ struct Smem {
   int flags[4];
 };
 
+// phase timing (debug builds only: -DRGB_CLUSTER_PROBE): ns per phase summed
+// over the run, for CTA 0 (home) and CTA 1, read back with rgb_cluster_probe()
+#ifdef RGB_CLUSTER_PROBE
+__device__ unsigned long long g_probe[2][16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE(i)                                                              \
+  do {                                                                        \
+    if (tid == 0 && c < 2) {                                                  \
+      const unsigned long long now_ = gtime();                                \
+      atomicAdd(&g_probe[c][i], now_ - probe_t);                              \
+      probe_t = now_;                                                         \
+    }                                                                         \
+  } while (0)
+#else
+#define PROBE(i) \
+  do {           \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
@@ -76,6 +99,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
                                                         int64_t T, uint8_t* __restrict__ blog,
                                                         double* __restrict__ clog) {
   constexpr int IT = R / 8, NXT = (R + 8) / 8, GX = R + 8, MT = TT / 8;
+  constexpr int NG = NW / MT;                 // warps per M tile
+  constexpr int NJ1 = (NXT + NG - 1) / NG;    // P1 N tiles per warp
+  constexpr int NJ3 = (CW / 8) / NG;          // P3 N tiles per warp
+  static_assert(NW % MT == 0 && (CW / 8) % NG == 0, "warp tiling");
   using SM = Smem<R, TT, TI>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SM& S = *reinterpret_cast<SM*>(smem_raw);
@@ -87,6 +114,9 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
   const bool home = (c == 0);
   const int64_t cid = blockIdx.x / ncl, ncid = gridDim.x / ncl;
   auto rem = [&](int u) { return cluster.map_shared_rank(&S, u); };
+#ifdef RGB_CLUSTER_PROBE
+  unsigned long long probe_t = gtime();
+#endif
 
   for (int64_t b = cid; b < cfg.num_streams; b += ncid) {
     int status = st.status[b];
@@ -146,15 +176,18 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       const bool in_t = base + p >= rs && base + p < te;
       // U = P G^T (M = i, N = t, K = i'): warp w owns rows 8w..8w+7
       {
-        double acc[2] = {0.0, 0.0};
+        double acc[2] = {0.0, 0.0}, acc2[2] = {0.0, 0.0};
         if (8 * w < r) {
-          for (int kt = 0; kt < kr; ++kt)
+          for (int kt = 0; kt < kr; kt += 2) {
             mma(acc, S.Ps[8 * w + p][4 * kt + q], in_t ? S.Gs[base + p][4 * kt + q] : 0.0);
+            if (kt + 1 < kr) mma(acc2, S.Ps[8 * w + p][4 * kt + 4 + q], in_t ? S.Gs[base + p][4 * kt + 4 + q] : 0.0);
+          }
         }
-        S.Ub[8 * w + p][2 * q] = acc[0];
-        S.Ub[8 * w + p][2 * q + 1] = acc[1];
+        S.Ub[8 * w + p][2 * q] = acc[0] + acc2[0];
+        S.Ub[8 * w + p][2 * q + 1] = acc[1] + acc2[1];
       }
       __syncthreads();
+      PROBE(10);
       if (w == 0) {
         // S = G U and G W (M = t, K = i), two chains each
         double s0[2] = {0.0, 0.0}, s1[2] = {0.0, 0.0}, g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
@@ -205,6 +238,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         S.Dy[p][2 * q + 1] = dh[1] * S.rd[p];
       }
       __syncthreads();
+      PROBE(11);
       // Y = U E^T (M = i, N = t, K = t'), W += Y (D^-1 E dy0) (M = i, N = cc, K = t)
       if (8 * w < r) {
         double yb[2] = {0.0, 0.0};
@@ -220,15 +254,19 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         S.Wb[8 * w + p][2 * q + 1] = wb[1];
       }
       __syncthreads();
+      PROBE(12);
       // P -= Y D^-1 Y^T (M = i, N = i', K = t): warp w owns row block w
       if (8 * w < r) {
         const double ys0 = -S.Yb[8 * w + p][q] * S.rd[q], ys1 = -S.Yb[8 * w + p][4 + q] * S.rd[4 + q];
-        for (int nt = 0; 8 * nt < r; ++nt) {
-          double acc[2] = {S.Ps[8 * w + p][8 * nt + 2 * q], S.Ps[8 * w + p][8 * nt + 2 * q + 1]};
-          mma(acc, ys0, S.Yb[8 * nt + p][q]);
-          mma(acc, ys1, S.Yb[8 * nt + p][4 + q]);
-          S.Ps[8 * w + p][8 * nt + 2 * q] = acc[0];
-          S.Ps[8 * w + p][8 * nt + 2 * q + 1] = acc[1];
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          if (8 * nt < r) {
+            double acc[2] = {S.Ps[8 * w + p][8 * nt + 2 * q], S.Ps[8 * w + p][8 * nt + 2 * q + 1]};
+            mma(acc, ys0, S.Yb[8 * nt + p][q]);
+            mma(acc, ys1, S.Yb[8 * nt + p][4 + q]);
+            S.Ps[8 * w + p][8 * nt + 2 * q] = acc[0];
+            S.Ps[8 * w + p][8 * nt + 2 * q + 1] = acc[1];
+          }
         }
       }
       // logs of the dependent rows
@@ -239,6 +277,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           for (int i = 0; i < R; ++i) clog[row * R + i] = S.Gs[base + tid][i];
       }
       __syncthreads();
+      PROBE(13);
     };
 
     int64_t consumed = 0;
@@ -251,25 +290,46 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       prefetch(pan + 1, s ^ 1);
       blk::cp_wait<1>();
       __syncthreads();
+      PROBE(9);
       int row_start = 0;
       while (true) {
         // ---- P1: G partial of my columns (M = t, N = i, K = my columns) ----------------
-        for (int pr = w; pr < MT * NXT; pr += NW) {
-          const int mt = pr / NXT, nt = pr % NXT;
-          double acc[2] = {0.0, 0.0};
-          if (nt >= IT || 8 * nt < r) {  // rows of C~ beyond the rank are zero
+        // warp w: M tile w % MT, N tiles w / MT + NG j -- independent MMA chains
+        // that share the A fragment of each K step
+        {
+          const int mt = w % MT, n0 = w / MT;
+          double acc[NJ1][2];
 #pragma unroll
-            for (int kt = 0; kt < CW / 4; ++kt)
-              mma(acc, (double)S.At[s][8 * mt + p][4 * kt + q], S.Ds[nt][kt][lane]);
+          for (int j = 0; j < NJ1; ++j) acc[j][0] = acc[j][1] = 0.0;
+          bool on[NJ1];
+#pragma unroll
+          for (int j = 0; j < NJ1; ++j) {
+            const int nt = n0 + NG * j;
+            on[j] = nt < NXT && (nt >= IT || 8 * nt < r);  // rows of C~ beyond the rank are zero
           }
-          *reinterpret_cast<double2*>(&S.Gp[(8 * mt + p) * GX + 8 * nt + 2 * q]) = make_double2(acc[0], acc[1]);
+#pragma unroll
+          for (int kt = 0; kt < CW / 4; ++kt) {
+            const double a = (double)S.At[s][8 * mt + p][4 * kt + q];
+#pragma unroll
+            for (int j = 0; j < NJ1; ++j)
+              if (on[j]) mma(acc[j], a, S.Ds[n0 + NG * j][kt][lane]);
+          }
+#pragma unroll
+          for (int j = 0; j < NJ1; ++j) {
+            const int nt = n0 + NG * j;
+            if (nt < NXT)
+              *reinterpret_cast<double2*>(&S.Gp[(8 * mt + p) * GX + 8 * nt + 2 * q]) = make_double2(acc[j][0], acc[j][1]);
+          }
         }
+        PROBE(0);
         cluster_sync_all();
+        PROBE(1);
         // ---- P2: G = sum of the partials; my chunk, stored into every CTA ---------------
         {
           constexpr int NE = TT * GX;
           const int chunk = (NE + ncl - 1) / ncl;
           const int e0 = c * chunk, e1 = (e0 + chunk < NE) ? e0 + chunk : NE;
+          // (DSMEM-bandwidth bound: 2 x 15/16 of an 18 KB panel of partials per CTA)
           for (int e = e0 + tid; e < e1; e += NT) {
             double v = 0.0;
             for (int u = 0; u < ncl; ++u) v += rem(u)->Gp[e];
@@ -277,31 +337,61 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
             for (int u = 0; u < ncl; ++u) rem(u)->Gs[t][i] = v;
           }
         }
+        PROBE(2);
         cluster_sync_all();
+        PROBE(3);
         // ---- P3: R = A - G C on my columns (M = t, N = my columns, K = i) ---------------
         {
           const int kmax = (r + 3) >> 2;
-          for (int pr = w; pr < MT * (CW / 8); pr += NW) {
-            const int mt = pr / (CW / 8), nt = pr % (CW / 8);
-            double acc[2] = {(double)S.At[s][8 * mt + p][8 * nt + 2 * q], (double)S.At[s][8 * mt + p][8 * nt + 2 * q + 1]};
-            for (int kt = 0; kt < kmax; ++kt) mma(acc, S.Gs[8 * mt + p][4 * kt + q], S.Cs[kt][nt][lane]);
-            *reinterpret_cast<double2*>(&S.Rs[8 * mt + p][8 * nt + 2 * q]) = make_double2(acc[0], acc[1]);
+          const int mt = w % MT, n0 = w / MT;  // warp w: M tile w % MT, N tiles w / MT + NG j
+          double acc[NJ3][2];
+#pragma unroll
+          for (int j = 0; j < NJ3; ++j) {
+            const int nt = n0 + NG * j;
+            acc[j][0] = (double)S.At[s][8 * mt + p][8 * nt + 2 * q];
+            acc[j][1] = (double)S.At[s][8 * mt + p][8 * nt + 2 * q + 1];
           }
+          for (int kt = 0; kt < kmax; ++kt) {
+            const double a = S.Gs[8 * mt + p][4 * kt + q];
+#pragma unroll
+            for (int j = 0; j < NJ3; ++j) mma(acc[j], a, S.Cs[kt][n0 + NG * j][lane]);
+          }
+#pragma unroll
+          for (int j = 0; j < NJ3; ++j)
+            *reinterpret_cast<double2*>(&S.Rs[8 * mt + p][8 * (n0 + NG * j) + 2 * q]) = make_double2(acc[j][0], acc[j][1]);
           __syncthreads();
           // |R_t|^2 and |a_t|^2 of my columns -> every CTA's nrm[c]
-          for (int t = w; t < TT; t += NW) {
-            const double r0 = S.Rs[t][lane], r1 = S.Rs[t][lane + 32];
-            const double a0 = (double)S.At[s][t][lane], a1 = (double)S.At[s][t][lane + 32];
-            const double rs2 = warp_sum(fma(r0, r0, r1 * r1));
-            const double as2 = warp_sum(fma(a0, a0, a1 * a1));
-            if (lane < ncl) {
-              SM* d = rem(lane);
-              d->nrm[c][0][t] = rs2;
-              d->nrm[c][1][t] = as2;
+          // NT / TT threads per row, each over every (NT / TT)-th column
+          constexpr int TPR = NT / TT;
+          static_assert(TPR >= 2 && (TPR & (TPR - 1)) == 0 && MAXCL <= 2 * TPR, "norm threads");
+          {
+            const int t = tid / TPR, part = tid % TPR;
+            double rs2 = 0.0, as2 = 0.0;
+#pragma unroll
+            for (int j = part; j < CW; j += TPR) {
+              const double rv = S.Rs[t][j], av = (double)S.At[s][t][j];
+              rs2 = fma(rv, rv, rs2);
+              as2 = fma(av, av, as2);
+            }
+#pragma unroll
+            for (int o = 1; o < TPR; o <<= 1) {
+              rs2 += __shfl_xor_sync(FULL, rs2, o);
+              as2 += __shfl_xor_sync(FULL, as2, o);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int u = part + h * TPR;
+              if (u < ncl) {
+                SM* d = rem(u);
+                d->nrm[c][0][t] = rs2;
+                d->nrm[c][1][t] = as2;
+              }
             }
           }
         }
+        PROBE(4);
         cluster_sync_all();
+        PROBE(5);
         // ---- P4: the rank test (identical in every CTA) --------------------------------
         if (w == 0) {
           double rsq = 0.0, asq = 0.0;
@@ -327,9 +417,12 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         __syncthreads();
         const int tstar = S.flags[0];
         const unsigned badm = (unsigned)S.flags[1];
+        PROBE(6);
         if (home && tstar > row_start) {
+          PROBE(14);
           for (int base = (row_start & ~7); base < tstar; base += 8) dep_block(s, base, row_start, tstar, t0);
         }
+        PROBE(7);
         if (tstar >= tv) break;
         if ((badm >> tstar) & 1u) {
           status |= RGB_ST_NONFINITE;
@@ -419,6 +512,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           }
         }
         __syncthreads();
+        PROBE(8);
         r += 1;
         row_start = tstar + 1;
         if (row_start >= tv) break;
@@ -522,3 +616,14 @@ int launch_cluster(const rgb_config& cfg, rgb_state& st, const void* rows, int64
 }
 
 }  // namespace rgb
+
+#ifdef RGB_CLUSTER_PROBE
+extern "C" int rgb_cluster_probe(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rgb::cls::g_probe, sizeof(rgb::cls::g_probe));
+  if (reset) {
+    unsigned long long z[2][16] = {};
+    cudaMemcpyToSymbol(rgb::cls::g_probe, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
