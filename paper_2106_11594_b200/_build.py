@@ -9,12 +9,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "librgb.so")
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC",
-    "-Xptxas", "-v",
-]
+ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMPILE_FLAGS = [*ARCH_FLAGS, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+NVCC_FLAGS = [*COMPILE_FLAGS, "-shared"]  # one-command form (documentation / debugging)
 
 
 def sources():
@@ -34,16 +31,38 @@ def stale():
 
 
 def build(force=False, log=None):
+    """Compile every csrc/*.cu to an object in parallel (-rdc off, whole-program
+    per file), then link librgb.so."""
     if not force and not stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((src, obj, [nvcc, *COMPILE_FLAGS, "-c", "-o", obj, src]))
+
+    def run(job):
+        return job, subprocess.run(job[2], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
+        results = list(pool.map(run, jobs))
+    link = [nvcc, *ARCH_FLAGS, "-shared", "-o", LIB, *[j[1] for j in jobs]]
+    lres = subprocess.run(link, capture_output=True, text=True) if all(r.returncode == 0 for _, r in results) else None
     if log is not None:
         with open(log, "w") as f:
-            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stderr[-4000:])
+            for job, res in results:
+                f.write(" ".join(job[2]) + "\n" + res.stdout + res.stderr)
+            if lres is not None:
+                f.write(" ".join(link) + "\n" + lres.stdout + lres.stderr)
+    for job, res in results:
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {os.path.basename(job[0])}:\n" + res.stderr[-4000:])
+    if lres.returncode != 0:
+        raise RuntimeError("nvcc link failed:\n" + lres.stderr[-4000:])
     return LIB
 
 

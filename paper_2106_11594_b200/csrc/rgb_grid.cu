@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, p = lane >> 2, q = lane & 3;
   const int nc = gridDim.x, c = blockIdx.x, c0 = c * CW;
   const int M = cfg.m, k = cfg.k;
+  const int rc = cfg.r_cap;   // stored rank capacity (<= R): global row stride of the factors
   const bool owner = c < IT;  // owns row block c of P and W
   double* ws_g = ws + 32;                          // [nc][TT][GX]
   double* ws_gf = ws_g + Ws<R, CW>::gpart(nc);     // [TT][GX]
@@ -115,9 +116,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     if (status) continue;
     int r = st.rank[b];
     const int64_t nobs0 = st.nobs[b];
-    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
-    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
-    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
+    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)rc * M;
+    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)rc * M;
+    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)rc * rc;
     double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
     const TI* Rb = rows + b * rstride;
     const TI* Yb = tgts + b * tstride;
@@ -126,17 +127,23 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     for (int e = tid; e < NXT * (CW / 4) * 32; e += NT) {
       const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
       const int i = 8 * nt + (l >> 2), col = c0 + 4 * kt + (l & 3);
-      double v = 0.0;
-      if (i < R) v = Dg[(int64_t)i * M + col];
-      else if (i - R < k) v = Xg[(int64_t)(i - R) * M + col];
+      double v = 0.0;  // rows past the capacity and columns past m are zero
+      if (col < M) {
+        if (i < rc) v = Dg[(int64_t)i * M + col];
+        else if (i >= R && i - R < k) v = Xg[(int64_t)(i - R) * M + col];
+      }
       S.Ds[nt][kt][l] = v;
     }
     for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
       const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
-      S.Cs[kt][nt][l] = -Cg[(int64_t)(4 * kt + (l & 3)) * M + c0 + 8 * nt + (l >> 2)];
+      const int i = 4 * kt + (l & 3), col = c0 + 8 * nt + (l >> 2);
+      S.Cs[kt][nt][l] = (i < rc && col < M) ? -Cg[(int64_t)i * M + col] : 0.0;
     }
     if (owner) {
-      for (int e = tid; e < 8 * R; e += NT) S.Ps[e / R][e % R] = Pg[(int64_t)(8 * c + e / R) * R + e % R];
+      for (int e = tid; e < 8 * R; e += NT) {
+        const int i = 8 * c + e / R, i2 = e % R;
+        S.Ps[e / R][i2] = (i < rc && i2 < rc) ? Pg[(int64_t)i * rc + i2] : 0.0;
+      }
       for (int e = tid; e < 64; e += NT) S.Wb[e >> 3][e & 7] = 0.0;
     }
     __syncthreads();
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       // tile rows of my columns and the targets
       for (int e = tid; e < TT * CW; e += NT) {
         const int t = e / CW, j = e % CW;
-        S.At[t][j] = t < tv ? (double)Rb[(t0 + t) * M + c0 + j] : 0.0;
+        S.At[t][j] = (t < tv && c0 + j < M) ? (double)Rb[(t0 + t) * M + c0 + j] : 0.0;
       }
       for (int e = tid; e < 64; e += NT) {
         const int t = e >> 3, cc = e & 7;
@@ -406,7 +413,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           consumed = t0 + tstar;
           break;
         }
-        if (r >= R) {
+        if (r >= rc) {
           status |= RGB_ST_RANK_CAP;
           stopped = true;
           consumed = t0 + tstar;
@@ -520,14 +527,19 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     // ---- write back: C~, C, P, W -> ws, then x = x0 + C~^T W on my columns ------------
     for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
       const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
-      Dg[(int64_t)(8 * nt + (l >> 2)) * M + c0 + 4 * kt + (l & 3)] = S.Ds[nt][kt][l];
+      const int i = 8 * nt + (l >> 2), col = c0 + 4 * kt + (l & 3);
+      if (i < rc && col < M) Dg[(int64_t)i * M + col] = S.Ds[nt][kt][l];
     }
     for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
       const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
-      Cg[(int64_t)(4 * kt + (l & 3)) * M + c0 + 8 * nt + (l >> 2)] = -S.Cs[kt][nt][l];
+      const int i = 4 * kt + (l & 3), col = c0 + 8 * nt + (l >> 2);
+      if (i < rc && col < M) Cg[(int64_t)i * M + col] = -S.Cs[kt][nt][l];
     }
     if (owner) {
-      for (int e = tid; e < 8 * R; e += NT) Pg[(int64_t)(8 * c + e / R) * R + e % R] = S.Ps[e / R][e % R];
+      for (int e = tid; e < 8 * R; e += NT) {
+        const int i = 8 * c + e / R, i2 = e % R;
+        if (i < rc && i2 < rc) Pg[(int64_t)i * rc + i2] = S.Ps[e / R][i2];
+      }
       for (int e = tid; e < 64; e += NT) ws_w[(size_t)(8 * c + (e >> 3)) * 8 + (e & 7)] = S.Wb[e >> 3][e & 7];
     }
     grid_sync(ctr, epoch);
@@ -536,7 +548,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       double x = S.Ds[NXT - 1][jl >> 2][4 * (cc) + (jl & 3)];  // x0^T row cc sits in the last N tile
       // the last N tile of Ds holds x0^T rows R..R+7: lane = 4 * (i - R) + (jl & 3)
       for (int i = 0; i < r; ++i) x = fma(S.Ds[i >> 3][jl >> 2][4 * (i & 7) + (jl & 3)], __ldcg(ws_w + (size_t)i * 8 + cc), x);
-      Xg[(int64_t)cc * M + c0 + jl] = x;
+      if (c0 + jl < M) Xg[(int64_t)cc * M + c0 + jl] = x;
     }
     if (c == 0 && tid == 0) {
       st.rank[b] = r;
@@ -553,12 +565,17 @@ template <int R, int CW, typename TI>
 static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                          const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                          cudaStream_t stream, int num_sms) {
-  const int nc = cfg.m / CW;
-  if (nc > num_sms || nc < R / 8) return RGB_E_UNSUPPORTED;
+  // CTA c owns columns [c CW, (c + 1) CW) (masked past m) and, for c < R / 8, a
+  // row block of P^-1 and W: enough CTAs for both, all co-resident (one per SM)
+  int nc = (cfg.m + CW - 1) / CW;
+  if (nc < R / 8) nc = R / 8;
+  if (nc > num_sms || cfg.r_cap > R) return RGB_E_UNSUPPORTED;
   auto kern = cfg.variant == RGB_GENERAL ? grd::grid_kernel<R, CW, true, TI> : grd::grid_kernel<R, CW, false, TI>;
   const size_t smem = sizeof(grd::GridSmem<R, CW>);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
     return RGB_E_UNSUPPORTED;
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, grd::NT, smem);
   if (per_sm < 1) return RGB_E_UNSUPPORTED;
@@ -580,24 +597,39 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
+// Single large streams of any width up to 148 x 16 columns and capacity up to
+// 512: the smallest instantiated R >= r_cap.  (Small problems stay on the
+// generic kernel: a grid step costs a few microseconds of barriers.)
 bool grid_supports(const rgb_config& cfg) {
   const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
                       (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
   if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
   if (cfg.num_streams > 4) return false;  // a handful of large streams, one after the other
-  return (cfg.m == 1024 && cfg.r_cap == 64) || (cfg.m == 2048 && cfg.r_cap == 512);
+  if (cfg.r_cap > 512 || cfg.m > 148 * 16) return false;
+  return (int64_t)cfg.m * cfg.r_cap >= 32768;
+}
+
+template <typename TI>
+static int launch_grid_r(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
+                         const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
+                         cudaStream_t stream, int num_sms) {
+  if (cfg.r_cap <= 64 && cfg.m <= 148 * 8)
+    return launch_grid_t<64, 8, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.r_cap <= 64)
+    return launch_grid_t<64, 16, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.r_cap <= 128)
+    return launch_grid_t<128, 16, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.r_cap <= 256)
+    return launch_grid_t<256, 16, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  return launch_grid_t<512, 16, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
 }
 
 int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
                 int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms, bool f32in) {
   if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;
-  if (cfg.m == 1024 && cfg.r_cap == 64)
-    return f32in ? launch_grid_t<64, 8, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
-                 : launch_grid_t<64, 8, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
-  if (cfg.m == 2048 && cfg.r_cap == 512)
-    return f32in ? launch_grid_t<512, 16, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
-                 : launch_grid_t<512, 16, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
-  return RGB_E_UNSUPPORTED;
+  if (!grid_supports(cfg)) return RGB_E_UNSUPPORTED;
+  return f32in ? launch_grid_r<float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+               : launch_grid_r<double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
 }
 
 }  // namespace rgb

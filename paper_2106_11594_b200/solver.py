@@ -221,7 +221,10 @@ class RecursiveSolver:
             T = n - done
             log_coords = bool(self._trackers)
             branch = torch.zeros((1, T), dtype=torch.uint8, device=dev)
-            resid = torch.zeros((1, T, 1), dtype=bs.dtype, device=dev)
+            # per-row residuals only for update() reports: requesting them
+            # routes the call to the generic kernel (the tensor-core kernels
+            # do not log them)
+            resid = torch.zeros((1, T, 1), dtype=bs.dtype, device=dev) if want_report else None
             coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=dev) if log_coords else None
             gain = torch.zeros((1, self._m), dtype=bs.dtype, device=dev) if want_report else None
             bs.ingest(rows[done:].view(1, T, self._m), tg[done:].view(1, T, 1), branch_log=branch,

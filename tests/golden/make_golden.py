@@ -118,5 +118,33 @@ def main():
             print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
+def bench_cells():
+    """Inputs of the reference's bench cells (bench.py:166-211) for two small
+    plans, plus the reference's solve_batch of each solve cell: pins the
+    cell-seeding of paper_2106_11594_b200.experiments."""
+    from rankrls import bench
+
+    out = {}
+    plan = bench.make_plan("rank-fixed-r", [16, 32], fixed_r=4, seed=7)
+    for i, (n, m, r) in enumerate(plan.grid):
+        A = matrices.random_standardized(n, m, r, bench._cell_seed(plan, i, 0))
+        y = np.random.default_rng(bench._cell_seed(plan, i, 1)).standard_normal(n)
+        x, rank = solver.solve_batch(A, y)
+        out.update({f"solve{i}_A": A, f"solve{i}_y": y, f"solve{i}_x": x, f"solve{i}_rank": rank})
+    plan = bench.make_plan("update-cost", [4, 8], fixed_m=32, seed=1)
+    for i, (r, m, _) in enumerate(plan.grid):
+        rng = np.random.default_rng(bench._cell_seed(plan, i, 0))
+        basis = rng.standard_normal((r, m))
+        yb = rng.standard_normal(r)
+        probes = rng.standard_normal((32, r)) @ basis
+        out.update({f"upd{i}_basis": basis, f"upd{i}_y": yb, f"upd{i}_probes": probes,
+                    f"upd{i}_targets": rng.standard_normal(32)})
+    np.savez_compressed(os.path.join(OUT, "bench_cells.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["bench"]:
+        bench_cells()
+    else:
+        main()
+        bench_cells()

@@ -705,3 +705,40 @@ def test_cluster_kernel_nonfinite_and_rank_cap():
     assert st[2] & 1 and bs.rank.cpu().numpy()[2] == 64
     o = oracle.ingest(rows[:1], tg[:1], r_cap=64, nthreads=1)
     assert relerr(bs.solution.cpu().numpy()[0], oracle.solution(o)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("m,r_cap,r,n,tol", [(2000, 512, 100, 260, 1e-9), (700, 128, 90, 200, 1e-9),
+                                             (2048, 64, 20, 300, 1e-9), (300, 256, 150, 170, 1e-9),
+                                             (512, 512, 512, 512, 1e-6)])
+def test_grid_kernel_any_width_and_capacity(m, r_cap, r, n, tol):
+    """The grid kernel serves any single large stream (m up to 2368, r_cap up
+    to 512; columns past m and factor rows past r_cap masked): branches, rank,
+    x and the stored factors against the oracle, including a full-rank square
+    system that fills the capacity exactly."""
+    rows, tg = _lowrank_streams(1, n, m, r, 2, seed=m + r)
+    res = run_batched(rows, tg, r_cap=r_cap)
+    o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=1)
+    assert int(o["rank"][0]) == r and o["status"][0] == 0
+    assert res["status"][0] == 0 and int(res["rank"][0]) == r
+    assert np.array_equal(res["branch"][0], o["branch"][0])
+    # square full rank: A = G1 G2 with two 512 x 512 Gaussian factors has
+    # cond 1.5e5 and the recursion itself leaves a 1e-5 residual there
+    # (oracle and reference alike), so two correct fp64 runs differ at ~1e-8
+    assert relerr(res["x"][0], oracle.solution(o)[0]) <= tol
+    bs = res["solver"]
+    assert relerr(bs.basis_t.cpu().numpy(), o["C"]) <= 1e-9
+    assert relerr(bs.dual_t.cpu().numpy(), o["D"]) <= 1e-6 if r == m else 1e-9
+
+
+def test_dropin_solver_large_width_grows_capacity_on_the_grid_kernel():
+    """RecursiveSolver (drop-in API) on a wide stream: the capacity doubles as
+    the rank grows (16 -> 512) on the grid kernel; the result equals the
+    oracle's and the reference's known behaviour (rank = construction rank)."""
+    from paper_2106_11594_b200 import RecursiveSolver
+
+    rows, tg = _lowrank_streams(1, 420, 2000, 300, 1, seed=5)
+    s = RecursiveSolver(2000)
+    s.ingest(rows[0], tg[0, :, 0])
+    o = oracle.ingest(rows, tg, r_cap=512, nthreads=1)
+    assert s.rank == int(o["rank"][0]) == 300
+    assert relerr(np.asarray(s.solution), oracle.solution(o)[0, :, 0]) <= 1e-9
