@@ -220,7 +220,7 @@ class RecursiveSolver:
         while done < n:
             T = n - done
             log_coords = bool(self._trackers)
-            branch = torch.zeros((1, T), dtype=torch.uint8, device=dev)
+            branch = torch.zeros((1, T), dtype=torch.uint8, device=dev) if want_report else None
             # per-row residuals only for update() reports: requesting them
             # routes the call to the generic kernel (the tensor-core kernels
             # do not log them)
@@ -229,17 +229,18 @@ class RecursiveSolver:
             gain = torch.zeros((1, self._m), dtype=bs.dtype, device=dev) if want_report else None
             bs.ingest(rows[done:].view(1, T, self._m), tg[done:].view(1, T, 1), branch_log=branch,
                       coords_log=coords, resid_log=resid, gain_out=gain)
-            nobs = int(bs.nobs_t[0].item())
+            # one device-to-host round trip for the three counters
+            nobs, rank, status = (int(v) for v in torch.cat(
+                [bs.nobs_t[:1], bs.rank_t[:1].long(), bs.status_t[:1].long()]).tolist())
             consumed = nobs - self._host["nobs"]
             self._host["nobs"] = nobs
-            self._host["rank"] = int(bs.rank_t[0].item())
+            self._host["rank"] = rank
             if log_coords and consumed:
                 self._coords_chunks.append(coords[0, :consumed].cpu().numpy())
             if want_report:
                 res = {"branch": branch[0, :consumed].cpu().numpy(), "resid": resid[0, :consumed, 0].cpu().numpy(),
                        "gain": gain[0].cpu().numpy()}
             done += consumed
-            status = int(bs.status_t[0].item())
             if status & _lib.ST_RANK_CAP:
                 bs.grow(2 * bs.r_cap)
                 bs.status_t.zero_()
