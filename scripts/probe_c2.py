@@ -28,7 +28,7 @@ for i in range(3):
     e1.record()
     torch.cuda.synchronize()
 lib.rgb_cluster_probe(buf.ctypes.data, 0)
-names = ["P1", "barA", "P2", "barB", "P3+norms", "barC", "P4", "dep-tail", "grow", "panel-load", "dep:U", "dep:S+LDL", "dep:Y+W", "dep:P", "dep-enter"]
+names = ["P1", "barA", "P2", "barB", "P3+norms", "barC", "P4", "-", "grow", "panel-load", "dep:U", "dep:S+LDL", "dep:Y+W", "dep:P", "wait-slot"]
 print("kernel ms", e0.elapsed_time(e1))
 for c in range(2):
-    print("CTA", c, {n: round(buf[c][i] / 1e6, 3) for i, n in enumerate(names)})
+    print(["column 0", "home"][c], {n: round(buf[c][i] / 1e6, 3) for i, n in enumerate(names)})
