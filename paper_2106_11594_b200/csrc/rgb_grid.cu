@@ -44,6 +44,29 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+// phase timing (debug builds only: -DRGB_GRID_PROBE): ns summed per phase for
+// CTA 0 and CTA 1, read back with rgb_grid_probe()
+#ifdef RGB_GRID_PROBE
+__device__ unsigned long long g_gprobe[2][16];
+__device__ __forceinline__ unsigned long long ggtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GPROBE(i)                                              \
+  do {                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 2) {                  \
+      const unsigned long long now_ = ggtime();                \
+      atomicAdd(&g_gprobe[blockIdx.x][i], now_ - probe_t);     \
+      probe_t = now_;                                          \
+    }                                                          \
+  } while (0)
+#else
+#define GPROBE(i) \
+  do {            \
+  } while (0)
+#endif
+
 // all CTAs of the (cooperative) grid; counter zeroed before the launch
 __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned& epoch) {
   __syncthreads();
@@ -109,6 +132,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
   double* ws_z = ws_w + (size_t)R * 8;             // [R]: z = P gamma (non-general growth)
   double* ws_d = ws_z + R;                         // [IT][16]: gamma.z, gamma^T W partials
   unsigned epoch = 0;
+#ifdef RGB_GRID_PROBE
+  unsigned long long probe_t = ggtime();
+#endif
   unsigned nproj = 0;  // projections so far (selects the ws_r buffer)
 
   for (int64_t b = 0; b < cfg.num_streams; ++b) {
@@ -170,18 +196,37 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         // test's reads of ws_r and the next projection's writes: alternate buffers
         double* ws_r = ws_r0 + (size_t)(nproj++ & 1u) * nc * 2 * TT;
         // ---- P1: G partial of my columns (M = t, N = i, K = my columns) -> ws
-        for (int nt = w; nt < NXT; nt += NW) {
-          double acc[2] = {0.0, 0.0};
+        // (N tiles past the rank are zero: skipped here, zeroed by the reducers)
+        const int nlive = (r + 7) >> 3;
+        for (int n0 = w; n0 < NXT; n0 += 4 * NW) {
+          double acc[4][2] = {};
+          bool on[4];
 #pragma unroll
-          for (int kt = 0; kt < CW / 4; ++kt) mma(acc, S.At[p][4 * kt + q], S.Ds[nt][kt][lane]);
-          *reinterpret_cast<double2*>(ws_g + ((size_t)c * TT + p) * GX + 8 * nt + 2 * q) = make_double2(acc[0], acc[1]);
+          for (int jj = 0; jj < 4; ++jj) {
+            const int nt = n0 + NW * jj;
+            on[jj] = nt < NXT && (nt >= IT || nt < nlive);
+          }
+#pragma unroll
+          for (int kt = 0; kt < CW / 4; ++kt) {
+            const double a = S.At[p][4 * kt + q];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+              if (on[jj]) mma(acc[jj], a, S.Ds[n0 + NW * jj][kt][lane]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (on[jj])
+              *reinterpret_cast<double2*>(ws_g + ((size_t)c * TT + p) * GX + 8 * (n0 + NW * jj) + 2 * q) =
+                  make_double2(acc[jj][0], acc[jj][1]);
         }
         if (tid < TT) {  // |a_t|^2 of my columns
           double s = 0.0;
           for (int j = 0; j < CW; ++j) s = fma(S.At[tid][j], S.At[tid][j], s);
           ws_r[((size_t)1 * TT + tid) * nc + c] = s;
         }
+        GPROBE(0);
         grid_sync(ctr, epoch);
+        GPROBE(1);
         // ---- P2: G = sum of the partials.  CTA c reduces a contiguous chunk of
         // elements: warp w reads partials u = w, w+8, ... (coalesced rows of
         // 32 elements), then the 8 warp sums are added in a fixed order.
@@ -189,14 +234,21 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           constexpr int NE = TT * GX;
           const int chunk = (NE + nc - 1) / nc;
           const int e0 = c * chunk, e1 = (e0 + chunk < NE) ? e0 + chunk : NE;
+          constexpr int MAXU = (148 + NW - 1) / NW;  // partials per warp (one CTA per SM)
           for (int eb = e0; eb < e1; eb += 32) {
             const int e = eb + lane;
-            double a4[4] = {0.0, 0.0, 0.0, 0.0};
-            if (e < e1) {
-#pragma unroll 4
-              for (int u = w; u < nc; u += NW) a4[(u >> 3) & 3] += __ldcg(ws_g + (size_t)u * NE + e);
+            const int col = e % GX;  // G column: coordinate i < R, or R + c for a.x0
+            const bool live = e < e1 && (col >= R || col < 8 * nlive);
+            double v[MAXU];  // every load in flight before the (fixed-order) sum
+#pragma unroll
+            for (int i = 0; i < MAXU; ++i) {
+              const int u = w + NW * i;
+              v[i] = (live && u < nc) ? __ldcg(ws_g + (size_t)u * NE + e) : 0.0;
             }
-            S.red[w][lane] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < MAXU; ++i) sum += v[i];
+            S.red[w][lane] = sum;
             __syncthreads();
             if (w == 0 && e < e1) {
               double v = 0.0;
@@ -206,19 +258,36 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             }
             __syncthreads();
           }
-        }        grid_sync(ctr, epoch);
+        }
+        GPROBE(2);
+        grid_sync(ctr, epoch);
+        GPROBE(3);
         for (int e = tid; e < TT * GX; e += NT) S.Gs[e / GX][e % GX] = __ldcg(ws_gf + e);
         __syncthreads();
         // ---- P3: R = A - G C on my columns (M = t, N = my columns, K = i split over warps)
         {
-          double acc[CW / 8][2];
+          double acc[CW / 8][2], acc2[CW / 8][2];
 #pragma unroll
-          for (int nt = 0; nt < CW / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+          for (int nt = 0; nt < CW / 8; ++nt) acc[nt][0] = acc[nt][1] = acc2[nt][0] = acc2[nt][1] = 0.0;
           const int kmax = (r + 3) >> 2;  // rows of C beyond the rank are zero
-          for (int kt = w; kt < kmax; kt += NW) {
+          int kt = w;
+          for (; kt + NW < kmax; kt += 2 * NW) {  // two independent chains
+            const double a = S.Gs[p][4 * kt + q], a2 = S.Gs[p][4 * (kt + NW) + q];
+#pragma unroll
+            for (int nt = 0; nt < CW / 8; ++nt) {
+              mma(acc[nt], a, S.Cs[kt][nt][lane]);
+              mma(acc2[nt], a2, S.Cs[kt + NW][nt][lane]);
+            }
+          }
+          if (kt < kmax) {
             const double a = S.Gs[p][4 * kt + q];
 #pragma unroll
             for (int nt = 0; nt < CW / 8; ++nt) mma(acc[nt], a, S.Cs[kt][nt][lane]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < CW / 8; ++nt) {
+            acc[nt][0] += acc2[nt][0];
+            acc[nt][1] += acc2[nt][1];
           }
 #pragma unroll
           for (int nt = 0; nt < CW / 8; ++nt) {
@@ -239,7 +308,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             ws_r[((size_t)0 * TT + tid) * nc + c] = s;
           }
         }
+        GPROBE(4);
         grid_sync(ctr, epoch);
+        GPROBE(5);
         // ---- P4: the rank test (identical in every CTA).  Warp t sums row t's
         // partials (lane l: CTAs l, l+32, ...; then a fixed butterfly).
         {
@@ -310,7 +381,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2 + 1) * 64 + p * 8 + 2 * q) = make_double2(gw[0], gw[1]);
             }
           }
+          GPROBE(6);
           grid_sync(ctr, epoch);
+          GPROBE(7);
           if (owner) {
             {
               // sums of the S and G W partials: warp w takes owners w, w+8, ...
@@ -386,16 +459,32 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               S.Wb[p][2 * q + 1] = wb[1];
             }
           }
+          GPROBE(8);
           grid_sync(ctr, epoch);
+          GPROBE(9);
           if (owner) {
             // P_b -= Y_b D^-1 Y^T (M = i in my block, N = i', K = t)
             const double ys0 = -S.Yb[p][q] * S.rd[q], ys1 = -S.Yb[p][4 + q] * S.rd[4 + q];
-            for (int nt = w; nt < IT; nt += NW) {
-              double acc[2] = {S.Ps[p][8 * nt + 2 * q], S.Ps[p][8 * nt + 2 * q + 1]};
-              mma(acc, ys0, __ldcg(ws_y + (size_t)(8 * nt + p) * TT + q));
-              mma(acc, ys1, __ldcg(ws_y + (size_t)(8 * nt + p) * TT + 4 + q));
-              S.Ps[p][8 * nt + 2 * q] = acc[0];
-              S.Ps[p][8 * nt + 2 * q + 1] = acc[1];
+            const int nlive = (r + 7) >> 3;  // row blocks of Y past the rank are zero
+            constexpr int NPW = (IT + NW - 1) / NW;
+            double y0[NPW], y1[NPW];  // every L2 load in flight first
+#pragma unroll
+            for (int i = 0; i < NPW; ++i) {
+              const int nt = w + NW * i;
+              const bool on = nt < nlive;
+              y0[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + q) : 0.0;
+              y1[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + 4 + q) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < NPW; ++i) {
+              const int nt = w + NW * i;
+              if (nt < nlive) {
+                double acc[2] = {S.Ps[p][8 * nt + 2 * q], S.Ps[p][8 * nt + 2 * q + 1]};
+                mma(acc, ys0, y0[i]);
+                mma(acc, ys1, y1[i]);
+                S.Ps[p][8 * nt + 2 * q] = acc[0];
+                S.Ps[p][8 * nt + 2 * q + 1] = acc[1];
+              }
             }
           }
           if (c == 0 && tid < TT && tid >= rs && tid < te) {
@@ -474,7 +563,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               ws_d[(size_t)c * 16 + tid] = v;
             }
           }
+          GPROBE(10);
           grid_sync(ctr, epoch);
+          GPROBE(11);
           const double resc = (cfg.variant == RGB_ORTHONORMAL) ? 1.0 / sqrt(rsq) : cfg.alpha;
           const double last = 1.0 / resc;
           const double alpha = 1.0 / last;
@@ -633,3 +724,14 @@ int launch_grid(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t 
 }
 
 }  // namespace rgb
+
+#ifdef RGB_GRID_PROBE
+extern "C" int rgb_grid_probe(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rgb::grd::g_gprobe, sizeof(rgb::grd::g_gprobe));
+  if (reset) {
+    unsigned long long z[2][16] = {};
+    cudaMemcpyToSymbol(rgb::grd::g_gprobe, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
