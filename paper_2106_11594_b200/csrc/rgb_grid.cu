@@ -262,7 +262,20 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         GPROBE(2);
         grid_sync(ctr, epoch);
         GPROBE(3);
-        for (int e = tid; e < TT * GX; e += NT) S.Gs[e / GX][e % GX] = __ldcg(ws_gf + e);
+        {  // the reduced G into shared memory: all of a thread's L2 loads in flight first
+          constexpr int PER = (TT * GX + NT - 1) / NT;
+          double v[PER];
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int e = tid + NT * i;
+            v[i] = e < TT * GX ? __ldcg(ws_gf + e) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            const int e = tid + NT * i;
+            if (e < TT * GX) S.Gs[e / GX][e % GX] = v[i];
+          }
+        }
         __syncthreads();
         // ---- P3: R = A - G C on my columns (M = t, N = my columns, K = i split over warps)
         {
@@ -314,11 +327,19 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         // ---- P4: the rank test (identical in every CTA).  Warp t sums row t's
         // partials (lane l: CTAs l, l+32, ...; then a fixed butterfly).
         {
+          constexpr int PER = (148 + 31) / 32;  // one CTA per SM
+          double rv[PER], av[PER];
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {  // [2][TT][nc]: coalesced, all in flight
+            const int u = lane + 32 * i;
+            rv[i] = u < nc ? __ldcg(ws_r + ((size_t)0 * TT + w) * nc + u) : 0.0;
+            av[i] = u < nc ? __ldcg(ws_r + ((size_t)1 * TT + w) * nc + u) : 0.0;
+          }
           double rs_ = 0.0, as_ = 0.0;
-#pragma unroll 4
-          for (int u = lane; u < nc; u += 32) {  // [2][TT][nc]: coalesced
-            rs_ += __ldcg(ws_r + ((size_t)0 * TT + w) * nc + u);
-            as_ += __ldcg(ws_r + ((size_t)1 * TT + w) * nc + u);
+#pragma unroll
+          for (int i = 0; i < PER; ++i) {
+            rs_ += rv[i];
+            as_ += av[i];
           }
           rs_ = warp_sum(rs_);
           as_ = warp_sum(as_);
@@ -388,13 +409,22 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             {
               // sums of the S and G W partials: warp w takes owners w, w+8, ...
               double a4[4] = {0.0, 0.0, 0.0, 0.0};
-              for (int u = w; u < IT; u += NW) {
-                const double2 s2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q));
-                const double2 g2 = __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q));
-                a4[0] += s2.x;
-                a4[1] += s2.y;
-                a4[2] += g2.x;
-                a4[3] += g2.y;
+              constexpr int PER = (IT + NW - 1) / NW;
+              double2 s2[PER], g2[PER];  // all in flight, then summed in owner order
+#pragma unroll
+              for (int i = 0; i < PER; ++i) {
+                const int u = w + NW * i;
+                s2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q))
+                               : make_double2(0.0, 0.0);
+                g2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q))
+                               : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+              for (int i = 0; i < PER; ++i) {
+                a4[0] += s2[i].x;
+                a4[1] += s2[i].y;
+                a4[2] += g2[i].x;
+                a4[3] += g2[i].y;
               }
 #pragma unroll
               for (int i = 0; i < 4; ++i) S.red[w][4 * lane + i] = a4[i];
