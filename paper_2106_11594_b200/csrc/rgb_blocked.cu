@@ -70,7 +70,8 @@ struct WarpSmem {
 // GEN: general variant only (the headline instantiation); !GEN: orthogonal /
 // orthonormal, whose grow step differs (solver.py:382-395)
 // TI: input element type (double, or float widened exactly on load)
-template <int M, int R, int KC, int WARPS, bool GEN, typename TI>
+// KM: k < KC right-hand sides (RHS lanes p >= k masked; KM = false is k = KC)
+template <int M, int R, int KC, int WARPS, bool GEN, typename TI, bool KM = false>
 __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
     const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
     double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
-    double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)KC * M;
+    const int kk_ = KM ? cfg.k : KC;  // right-hand sides (targets stride, X rows)
+    double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)kk_ * M;
     const TI* Rb = rows + b * rstride;
     const TI* Yb = tgts + b * tstride;
 
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // x0 = the solution at call start; when it is exactly zero a.x0 = 0 and
     // its contraction is skipped.
     bool nz = false;
-    if (!fresh) {
+    if (!fresh && (!KM || p < kk_)) {
 #pragma unroll
       for (int J = 0; J < JK / 2; ++J) {
         double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q);
@@ -156,8 +158,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int64_t ty = t0 + 2 * q + e;
-          const bool oky = ty < T;
-          cp_async_one<TI>(&S.Yt[s][lane][e], oky ? Yb + ty * KC + p : Yb, oky);
+          const bool oky = ty < T && (!KM || p < kk_);
+          cp_async_one<TI>(&S.Yt[s][lane][e], oky ? Yb + ty * kk_ + p : Yb, oky);
         }
       }
       cp_commit();
@@ -297,7 +299,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         double acc[2] = {0.0, 0.0};
 #pragma unroll
         for (int J = 0; J < JK / 2; ++J) {
-          const double2 xv = __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q));
+          const double2 xv = (!KM || p < kk_) ? __ldg(reinterpret_cast<const double2*>(Xg + p * M + 8 * J + 2 * q))
+                                              : make_double2(0.0, 0.0);
           const double2 v = slot(As, J * 32);
           mma(acc, xv.x, v.x);
           mma(acc, xv.y, v.y);
@@ -772,14 +775,14 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 #pragma unroll
     for (int jt = 0; jt < JT; ++jt) {
       double acc[2] = {0.0, 0.0};
-      if (has_x0) {
+      if (has_x0 && (!KM || p < kk_)) {
         const double2 v = *reinterpret_cast<const double2*>(Xg + p * M + 8 * jt + 2 * q);
         acc[0] = v.x;
         acc[1] = v.y;
       }
 #pragma unroll
       for (int kt = 0; kt < IK; ++kt) mma(acc, Wt[kt >> 1][kt & 1], Dm[sigma(kt, q) * DS + 8 * jt + p]);
-      *reinterpret_cast<double2*>(Xg + p * M + 8 * jt + 2 * q) = make_double2(acc[0], acc[1]);
+      if (!KM || p < kk_) *reinterpret_cast<double2*>(Xg + p * M + 8 * jt + 2 * q) = make_double2(acc[0], acc[1]);
     }
 #pragma unroll
     for (int mt = 0; mt < IT; ++mt)
@@ -811,21 +814,18 @@ bool blocked_supports(const rgb_config& cfg) {
   // reference, solver.py:364-365) is left to the generic kernel's status path
   const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
                       (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
-  return cfg.dtype == RGB_F64 && var_ok && cfg.m == BM && cfg.r_cap == BR && cfg.k == BK;
+  return cfg.dtype == RGB_F64 && var_ok && cfg.m == BM && cfg.r_cap == BR && cfg.k >= 1 && cfg.k <= BK;
 }
 
-template <typename TI>
+template <typename TI, bool KM>
 static int launch_blocked_t(const rgb_config& cfg, rgb_state& st, const TI* rows, int64_t rows_stride,
                             const TI* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                             cudaStream_t stream, int num_sms) {
   const bool gen = cfg.variant == RGB_GENERAL;
-  auto kern = gen ? blk::blocked_kernel<BM, BR, BK, BWARPS, true, TI> : blk::blocked_kernel<BM, BR, BK, BWARPS, false, TI>;
+  auto kern = gen ? blk::blocked_kernel<BM, BR, BK, BWARPS, true, TI, KM>
+                  : blk::blocked_kernel<BM, BR, BK, BWARPS, false, TI, KM>;
   const size_t smem = sizeof(blk::WarpSmem<BM, BR, BK, TI>) * BWARPS;
-  static bool attr[2] = {false, false};
-  if (!attr[gen]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[gen] = true;
-  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BWARPS * 32, smem);
   if (per_sm < 1) per_sm = 1;
@@ -841,11 +841,16 @@ int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms, bool f32in) {
   if (logs.resid || logs.gain) return RGB_E_UNSUPPORTED;  // per-row residuals: generic kernel
+  const bool km = cfg.k < BK;
   if (f32in)
-    return launch_blocked_t(cfg, st, (const float*)rows, rows_stride, (const float*)targets, tg_stride, T, logs,
-                            stream, num_sms);
-  return launch_blocked_t(cfg, st, (const double*)rows, rows_stride, (const double*)targets, tg_stride, T, logs,
-                          stream, num_sms);
+    return km ? launch_blocked_t<float, true>(cfg, st, (const float*)rows, rows_stride, (const float*)targets,
+                                              tg_stride, T, logs, stream, num_sms)
+              : launch_blocked_t<float, false>(cfg, st, (const float*)rows, rows_stride, (const float*)targets,
+                                               tg_stride, T, logs, stream, num_sms);
+  return km ? launch_blocked_t<double, true>(cfg, st, (const double*)rows, rows_stride, (const double*)targets,
+                                             tg_stride, T, logs, stream, num_sms)
+            : launch_blocked_t<double, false>(cfg, st, (const double*)rows, rows_stride, (const double*)targets,
+                                              tg_stride, T, logs, stream, num_sms);
 }
 
 }  // namespace rgb

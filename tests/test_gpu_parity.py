@@ -742,3 +742,34 @@ def test_dropin_solver_large_width_grows_capacity_on_the_grid_kernel():
     o = oracle.ingest(rows, tg, r_cap=512, nthreads=1)
     assert s.rank == int(o["rank"][0]) == 300
     assert relerr(np.asarray(s.solution), oracle.solution(o)[0, :, 0]) <= 1e-9
+
+
+@pytest.mark.parametrize("k", [1, 3, 7])
+def test_one_warp_kernel_fewer_right_hand_sides(k):
+    """Config-5-shaped streams with k < 8 right-hand sides stay on the one-warp
+    tensor-core kernel (the unused RHS lanes masked): branches, ranks and x
+    against the oracle, in one call and as two continuation calls (x0 != 0)."""
+    from paper_2106_11594_b200 import workloads
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    rows, tg = workloads.host_batch("c5", list(range(40)), n=300)
+    tg = np.ascontiguousarray(tg[..., :k])
+    o = oracle.ingest(rows, tg, r_cap=16, nthreads=8)
+    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0))
+    for split in (None, 133):
+        bs = BatchedSolver(40, 64, k=k, r_cap=16)
+        br = torch.zeros((40, 300), dtype=torch.uint8, device="cuda")
+        if split is None:
+            bs.ingest(dev(rows), dev(tg), branch_log=br)
+        else:
+            b1 = torch.zeros((40, split), dtype=torch.uint8, device="cuda")
+            b2 = torch.zeros((40, 300 - split), dtype=torch.uint8, device="cuda")
+            bs.ingest(dev(rows[:, :split]), dev(tg[:, :split]), branch_log=b1)
+            bs.ingest(dev(rows[:, split:]), dev(tg[:, split:]), branch_log=b2)
+            br = torch.cat([b1, b2], dim=1)
+        torch.cuda.synchronize()
+        assert np.array_equal(br.cpu().numpy()[ok], o["branch"][ok])
+        assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
+        X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
+        assert X.shape == (40, 64, k)
+        assert max(relerr(X[b], XO[b]) for b in np.nonzero(ok)[0]) <= 1e-10
