@@ -5,12 +5,13 @@ Workload (BASELINE.json configs[4], "C5"): B = 65536 independent streams,
 n = 1024 rows each, m = 64 regressors, rank 16 (A_b = G1_b G2_b; even b
 Gaussian factors, odd b integer factors in {-3..3}), k = 8 right-hand sides,
 fp64.  One step = solve every stream from scratch (state reset + one pass of
-the hot path over all n rows of all streams).  Streams are sharded over the
-ranks in contiguous blocks with no collective in the hot path ("weak" per
-stream, total work fixed -> "strong" scaling).
+the hot path over all n rows of all streams).  Weak scaling: each of N GPUs
+folds its own 65 536 streams -- contiguous blocks of one global set of
+N x 65 536, no collective on the data path; the single-stream configs (rows
+strictly sequential) run one replica per GPU.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c3|c1|c2|c4]
-                  [--dtype fp64|fp32] [--impl ours|reference]
+                  [--dtype fp64|fp32|fp32-state] [--impl ours|reference]
 
 `--impl reference` times the CPU oracle port (oracle/rgb_oracle.c, the C
 restatement of rankrls' ingest) on the host cores on a bounded sample of the
@@ -260,9 +261,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_total / v,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if args.dtype == "fp32-state" else "f64", "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d))",
-        "config": {"workload": args.config, "streams": cfg.streams, "n": cfg.n, "m": cfg.m, "k": cfg.k,
+        "config": {"workload": args.config, "streams": cfg.streams, "streams_per_gpu": cfg.streams, "n": cfg.n,
+                   "m": cfg.m, "k": cfg.k,
                    "rank": cfg.r, "sampled_streams": rows.shape[0]},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -293,7 +295,11 @@ def run_ours(args):
         else:
             dist.init_process_group("gloo")
     cfg = workloads.CONFIGS[args.config]
-    B = args.streams or cfg.streams
+    # weak scaling: every GPU folds its own per_gpu streams of one global set of
+    # world * per_gpu (ranks take contiguous blocks of global stream ids, no
+    # collective on the data path); single-stream configs run one replica per GPU
+    per_gpu = args.streams or cfg.streams
+    B = per_gpu * world
     b0, b1 = sharding.shard_range(B, world, rank)
     S = b1 - b0
     tdtype = torch.float64 if args.dtype == "fp64" else torch.float32   # inputs
@@ -428,9 +434,10 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32-state" else "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.dtype == "fp32-state" else "f64",
             "data": "synthetic: seeded A = G1 G2 per stream generated on device (SURVEY.md 8(d)); inputs resident in HBM",
-            "config": {"workload": args.config, "streams": B, "n": n, "m": cfg.m, "rank": cfg.r, "k": cfg.k,
+            "config": {"workload": args.config, "streams": B, "streams_per_gpu": per_gpu, "n": n, "m": cfg.m,
+                       "rank": cfg.r, "k": cfg.k,
                        "r_cap": cfg.r_cap, "variant": "general",
                        "eps": "auto" if args.eps is None else f"fixed {args.eps:g}",
                        "inputs": {"fp64": "fp64", "fp32": "fp32, widened exactly into the fp64 state on load",
@@ -438,7 +445,8 @@ def run_ours(args):
                        "l2": (f"inputs {in_bytes * world / 1e6:.0f} MB < 2x L2: L2 flushed (512 MB write) between "
                               "steps, outside the per-step events" if flush else
                               f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)"),
-                       "sharding": f"{S} contiguous streams per GPU, no collective"},
+                       "sharding": (f"{S} contiguous streams per GPU of {B}, no collective" if cfg.streams > 1 else
+                                    "single stream: one replica per GPU (rows are sequential; replicas only)")},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
                          "traffic": ncu_traffic(args.config, args.dtype),
