@@ -16,14 +16,6 @@ __device__ __forceinline__ void mma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// predicated form: the MMA is issued only when `on` (no branch, no divergence
-// of the register allocation between the two cases)
-__device__ __forceinline__ void mma_if(double (&d)[2], double a, double b, bool on) {
-  asm("{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
-      " @pp mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n}\n"
-      : "+d"(d[0]), "+d"(d[1])
-      : "d"(a), "d"(b), "r"((int)on));
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
