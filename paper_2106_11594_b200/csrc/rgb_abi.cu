@@ -137,9 +137,11 @@ static int ingest_impl(const rgb_config* cfg, rgb_state* st, const void* rows, i
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::blocked_wg_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
-  else if (rgb::cluster_supports(*cfg) && !lg.resid && !lg.gain)
+  // the multi-SM kernels pay microseconds of setup and barriers per call: a
+  // call of a few rows (a per-row update()) is faster on the generic kernel
+  else if (rgb::cluster_supports(*cfg) && T >= 8 && !lg.resid && !lg.gain)
     rc = rgb::launch_cluster(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
-  if (rc == RGB_E_UNSUPPORTED && rgb::grid_supports(*cfg) && !lg.resid && !lg.gain)
+  if (rc == RGB_E_UNSUPPORTED && rgb::grid_supports(*cfg) && T >= 8 && !lg.resid && !lg.gain)
     rc = rgb::launch_grid(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   if (rc == RGB_E_UNSUPPORTED)
     rc = rgb::launch_generic(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);

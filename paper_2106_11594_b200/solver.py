@@ -208,38 +208,80 @@ class RecursiveSolver:
             self._run(A, y, want_report=False)
 
     # -- device plumbing --------------------------------------------------------
+    def _buffers(self, n):
+        """Pinned host staging and device buffers for calls of up to n rows,
+        reused across calls (a per-row update() is latency bound: one H2D copy,
+        one launch, one set of async D2H copies and one synchronisation)."""
+        torch = self._torch
+        buf = getattr(self, "_buf", None)
+        if buf is not None and buf["cap"] >= n:
+            return buf
+        cap = 1 << max(0, (n - 1).bit_length())
+        dev, dt, m = self._bs.device, self._bs.dtype, self._m
+        buf = {
+            "cap": cap,
+            "rows_h": torch.empty((cap, m), dtype=dt, pin_memory=True),
+            "y_h": torch.empty((cap,), dtype=dt, pin_memory=True),
+            "rows_d": torch.empty((cap, m), dtype=dt, device=dev),
+            "y_d": torch.empty((cap,), dtype=dt, device=dev),
+            "branch_d": torch.empty((1, cap), dtype=torch.uint8, device=dev),
+            "resid_d": torch.empty((1, cap, 1), dtype=dt, device=dev),
+            "gain_d": torch.empty((1, m), dtype=dt, device=dev),
+            "branch_h": torch.empty((cap,), dtype=torch.uint8, pin_memory=True),
+            "resid_h": torch.empty((cap,), dtype=dt, pin_memory=True),
+            "gain_h": torch.empty((m,), dtype=dt, pin_memory=True),
+            "nobs_h": torch.empty((1,), dtype=torch.int64, pin_memory=True),
+            "cnt_h": torch.empty((2,), dtype=torch.int32, pin_memory=True),
+        }
+        self._buf = buf
+        return buf
+
     def _run(self, A, y, want_report):
         torch = self._torch
         bs = self._bs
-        dev = bs.device
         n = A.shape[0]
-        rows = torch.as_tensor(np.ascontiguousarray(A, dtype=self._kind.dtype), device=dev)
-        tg = torch.as_tensor(np.ascontiguousarray(y, dtype=self._kind.dtype), device=dev)
+        buf = self._buffers(n)
+        m = self._m
+        buf["rows_h"][:n].numpy()[...] = A
+        buf["y_h"][:n].numpy()[...] = y
+        stream = torch.cuda.current_stream(bs.device)
+        rows, tg = buf["rows_d"], buf["y_d"]
+        rows[:n].copy_(buf["rows_h"][:n], non_blocking=True)
+        tg[:n].copy_(buf["y_h"][:n], non_blocking=True)
         done = 0
         res = {}
         while done < n:
             T = n - done
             log_coords = bool(self._trackers)
-            branch = torch.zeros((1, T), dtype=torch.uint8, device=dev) if want_report else None
             # per-row residuals only for update() reports: requesting them
             # routes the call to the generic kernel (the tensor-core kernels
-            # do not log them)
-            resid = torch.zeros((1, T, 1), dtype=bs.dtype, device=dev) if want_report else None
-            coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=dev) if log_coords else None
-            gain = torch.zeros((1, self._m), dtype=bs.dtype, device=dev) if want_report else None
-            bs.ingest(rows[done:].view(1, T, self._m), tg[done:].view(1, T, 1), branch_log=branch,
+            # do not log them); every log entry of a consumed row is written
+            branch = buf["branch_d"][:, :T] if want_report else None
+            resid = buf["resid_d"][:, :T] if want_report else None
+            gain = buf["gain_d"] if want_report else None
+            coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=bs.device) if log_coords else None
+            bs.ingest(rows[done:n].view(1, T, m), tg[done:n].view(1, T, 1), branch_log=branch,
                       coords_log=coords, resid_log=resid, gain_out=gain)
-            # one device-to-host round trip for the three counters
-            nobs, rank, status = (int(v) for v in torch.cat(
-                [bs.nobs_t[:1], bs.rank_t[:1].long(), bs.status_t[:1].long()]).tolist())
+            # counters and report: asynchronous copies into pinned memory, one sync
+            buf["nobs_h"].copy_(bs.nobs_t[:1], non_blocking=True)
+            buf["cnt_h"][0:1].copy_(bs.rank_t[:1], non_blocking=True)
+            buf["cnt_h"][1:2].copy_(bs.status_t[:1], non_blocking=True)
+            if want_report:
+                buf["branch_h"][:T].copy_(branch[0], non_blocking=True)
+                buf["resid_h"][:T].copy_(resid[0, :, 0], non_blocking=True)
+                buf["gain_h"].copy_(gain[0], non_blocking=True)
+            stream.synchronize()
+            nobs = int(buf["nobs_h"][0])
+            rank, status = (int(v) for v in buf["cnt_h"].tolist())
             consumed = nobs - self._host["nobs"]
             self._host["nobs"] = nobs
             self._host["rank"] = rank
             if log_coords and consumed:
                 self._coords_chunks.append(coords[0, :consumed].cpu().numpy())
             if want_report:
-                res = {"branch": branch[0, :consumed].cpu().numpy(), "resid": resid[0, :consumed, 0].cpu().numpy(),
-                       "gain": gain[0].cpu().numpy()}
+                res = {"branch": buf["branch_h"][:consumed].numpy().copy(),
+                       "resid": buf["resid_h"][:consumed].numpy().copy(),
+                       "gain": buf["gain_h"].numpy().copy()}
             done += consumed
             if status & _lib.ST_RANK_CAP:
                 bs.grow(2 * bs.r_cap)
