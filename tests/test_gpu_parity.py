@@ -773,3 +773,17 @@ def test_one_warp_kernel_fewer_right_hand_sides(k):
         X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
         assert X.shape == (40, 64, k)
         assert max(relerr(X[b], XO[b]) for b in np.nonzero(ok)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,r_cap,streams,n", [("c5", 16, 64, 512), ("c3", 32, 16, 512), ("c2", 64, 1, 1024),
+                                                 ("c4", 512, 1, 700)])
+def test_runs_are_bitwise_deterministic(cfg, r_cap, streams, n):
+    """Every reduction runs in a fixed order (no floating-point atomics), so
+    repeated runs -- and the multi-SM kernels' cross-CTA sums -- give the same
+    bits: the branch log, the rank and x are identical run to run."""
+    rows, tg = _shape_rows(cfg, list(range(streams)), n)
+    a = run_batched(rows, tg, r_cap=r_cap)
+    b = run_batched(rows, tg, r_cap=r_cap)
+    assert np.array_equal(a["branch"], b["branch"]) and np.array_equal(a["rank"], b["rank"])
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(a["solver"].gram_t.cpu().numpy(), b["solver"].gram_t.cpu().numpy())
