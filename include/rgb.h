@@ -134,6 +134,12 @@ int rgb_project(const rgb_config *cfg, const rgb_state *state, const void *rows,
 int rgb_pinv(const rgb_config *cfg, const rgb_state *state, const void *coords, int64_t n,
              void *out, void *stream);
 
+/* Asynchronous copy of `bytes` between host (pinned) and device memory on the
+ * stream (direction inferred from the unified address space), for FFI callers
+ * that stage rows and read results without a CUDA runtime binding of their own
+ * -- the drop-in solver's per-row update() path uses it. */
+int rgb_memcpy_async(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Covariance V = A+ A+^T = C~^T P^-1 C~ (CovarianceTracker.covariance,
  * tracking.py:88-119; identity of test_tracking.py:188-198): out [B][m][m]. */
 int rgb_covariance(const rgb_config *cfg, const rgb_state *state, void *out, void *stream);

@@ -22,6 +22,7 @@ OK, E_INVALID, E_UNSUPPORTED, E_CUDA = 0, -1, -2, -3
 ST_RANK_CAP, ST_NONFINITE, ST_BAD_ALPHA = 1, 2, 4
 
 EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest", "rgb_ingest_f32in",
+           "rgb_memcpy_async",
            "rgb_project", "rgb_pinv", "rgb_covariance")
 
 
@@ -87,6 +88,7 @@ def load():
     lib.rgb_project.argtypes = [cfgp, stp, vp, vp, vp, vp, vp, vp]
     lib.rgb_pinv.argtypes = [cfgp, stp, vp, i64, vp, vp]
     lib.rgb_covariance.argtypes = [cfgp, stp, vp, vp]
+    lib.rgb_memcpy_async.argtypes = [vp, vp, i64, vp]
     for name in EXPORTS[2:]:
         getattr(lib, name).restype = ctypes.c_int
     if lib.rgb_abi_version() != RGB_ABI_VERSION:

@@ -194,6 +194,13 @@ int rgb_pinv(const rgb_config* cfg, const rgb_state* st, const void* coords, int
   return RGB_OK;
 }
 
+int rgb_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(RGB_E_INVALID, "rgb_memcpy_async: bad arguments");
+  if (bytes == 0) return RGB_OK;
+  const cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+  return e == cudaSuccess ? RGB_OK : cuda_fail(e, "rgb_memcpy_async");
+}
+
 int rgb_covariance(const rgb_config* cfg, const rgb_state* st, void* out, void* stream) {
   int rc = check_cfg(cfg);
   if (rc) return rc;

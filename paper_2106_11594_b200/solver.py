@@ -21,6 +21,7 @@ Differences, all deliberate and documented in DESIGN.md:
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -131,6 +132,7 @@ class RecursiveSolver:
                                  eps=None if eps.mode == "auto" else eps.value,
                                  alpha=float(alpha), dtype=tdtype, device=device)
         self._torch = torch
+        self._f32in = False
         self._host = {"rank": 0, "nobs": 0}
 
     # -- read-only access ---------------------------------------------------
@@ -210,16 +212,17 @@ class RecursiveSolver:
     # -- device plumbing --------------------------------------------------------
     def _buffers(self, n):
         """Pinned host staging and device buffers for calls of up to n rows,
-        reused across calls (a per-row update() is latency bound: one H2D copy,
-        one launch, one set of async D2H copies and one synchronisation)."""
+        reused across calls.  A per-row update() is latency bound, so a call is
+        one host-to-device copy per input, one ingest, asynchronous copies of
+        the counters and the report into pinned memory and one synchronisation,
+        all through raw pointers (librgb's rgb_memcpy_async)."""
         torch = self._torch
         buf = getattr(self, "_buf", None)
         if buf is not None and buf["cap"] >= n:
             return buf
         cap = 1 << max(0, (n - 1).bit_length())
         dev, dt, m = self._bs.device, self._bs.dtype, self._m
-        buf = {
-            "cap": cap,
+        t = {
             "rows_h": torch.empty((cap, m), dtype=dt, pin_memory=True),
             "y_h": torch.empty((cap,), dtype=dt, pin_memory=True),
             "rows_d": torch.empty((cap, m), dtype=dt, device=dev),
@@ -233,21 +236,37 @@ class RecursiveSolver:
             "nobs_h": torch.empty((1,), dtype=torch.int64, pin_memory=True),
             "cnt_h": torch.empty((2,), dtype=torch.int32, pin_memory=True),
         }
+        buf = {"cap": cap, "t": t, "esz": t["y_h"].element_size()}
+        buf.update({k + "_np": v.numpy() for k, v in t.items() if not k.endswith("_d")})
+        buf.update({k + "_p": v.data_ptr() for k, v in t.items()})
         self._buf = buf
         return buf
+
+    def _structs(self):
+        """rgb_config / rgb_state of the single stream, rebuilt when the capacity grows."""
+        bs = self._bs
+        key = (bs.r_cap, bs.basis_t.data_ptr())
+        if getattr(self, "_st_key", None) != key:
+            self._st = (bs.config(), bs.state())
+            self._st_key = key
+        return self._st
 
     def _run(self, A, y, want_report):
         torch = self._torch
         bs = self._bs
+        lib = bs.lib
         n = A.shape[0]
-        buf = self._buffers(n)
         m = self._m
-        buf["rows_h"][:n].numpy()[...] = A
-        buf["y_h"][:n].numpy()[...] = y
+        buf = self._buffers(n)
+        esz = buf["esz"]
+        buf["rows_h_np"][:n] = A
+        buf["y_h_np"][:n] = y
         stream = torch.cuda.current_stream(bs.device)
-        rows, tg = buf["rows_d"], buf["y_d"]
-        rows[:n].copy_(buf["rows_h"][:n], non_blocking=True)
-        tg[:n].copy_(buf["y_h"][:n], non_blocking=True)
+        h = ctypes.c_void_p(stream.cuda_stream)
+        cp = lib.rgb_memcpy_async
+        _lib.check(cp(buf["rows_d_p"], buf["rows_h_p"], n * m * esz, h), "rgb_memcpy_async")
+        _lib.check(cp(buf["y_d_p"], buf["y_h_p"], n * esz, h), "rgb_memcpy_async")
+        ingest = lib.rgb_ingest_f32in if self._f32in else lib.rgb_ingest
         done = 0
         res = {}
         while done < n:
@@ -256,32 +275,34 @@ class RecursiveSolver:
             # per-row residuals only for update() reports: requesting them
             # routes the call to the generic kernel (the tensor-core kernels
             # do not log them); every log entry of a consumed row is written
-            branch = buf["branch_d"][:, :T] if want_report else None
-            resid = buf["resid_d"][:, :T] if want_report else None
-            gain = buf["gain_d"] if want_report else None
             coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=bs.device) if log_coords else None
-            bs.ingest(rows[done:n].view(1, T, m), tg[done:n].view(1, T, 1), branch_log=branch,
-                      coords_log=coords, resid_log=resid, gain_out=gain)
+            logs = _lib.Logs(buf["branch_d_p"] if want_report else None,
+                             coords.data_ptr() if log_coords else None,
+                             buf["resid_d_p"] if want_report else None,
+                             buf["gain_d_p"] if want_report else None)
+            cfg, st = self._structs()
+            _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["rows_d_p"] + done * m * esz, T * m,
+                              buf["y_d_p"] + done * esz, T, T, ctypes.byref(logs), h), "rgb_ingest")
             # counters and report: asynchronous copies into pinned memory, one sync
-            buf["nobs_h"].copy_(bs.nobs_t[:1], non_blocking=True)
-            buf["cnt_h"][0:1].copy_(bs.rank_t[:1], non_blocking=True)
-            buf["cnt_h"][1:2].copy_(bs.status_t[:1], non_blocking=True)
+            _lib.check(cp(buf["nobs_h_p"], bs.nobs_t.data_ptr(), 8, h), "rgb_memcpy_async")
+            _lib.check(cp(buf["cnt_h_p"], bs.rank_t.data_ptr(), 4, h), "rgb_memcpy_async")
+            _lib.check(cp(buf["cnt_h_p"] + 4, bs.status_t.data_ptr(), 4, h), "rgb_memcpy_async")
             if want_report:
-                buf["branch_h"][:T].copy_(branch[0], non_blocking=True)
-                buf["resid_h"][:T].copy_(resid[0, :, 0], non_blocking=True)
-                buf["gain_h"].copy_(gain[0], non_blocking=True)
+                _lib.check(cp(buf["branch_h_p"], buf["branch_d_p"], T, h), "rgb_memcpy_async")
+                _lib.check(cp(buf["resid_h_p"], buf["resid_d_p"], T * esz, h), "rgb_memcpy_async")
+                _lib.check(cp(buf["gain_h_p"], buf["gain_d_p"], m * esz, h), "rgb_memcpy_async")
             stream.synchronize()
-            nobs = int(buf["nobs_h"][0])
-            rank, status = (int(v) for v in buf["cnt_h"].tolist())
+            nobs = int(buf["nobs_h_np"][0])
+            rank, status = int(buf["cnt_h_np"][0]), int(buf["cnt_h_np"][1])
             consumed = nobs - self._host["nobs"]
             self._host["nobs"] = nobs
             self._host["rank"] = rank
             if log_coords and consumed:
                 self._coords_chunks.append(coords[0, :consumed].cpu().numpy())
             if want_report:
-                res = {"branch": buf["branch_h"][:consumed].numpy().copy(),
-                       "resid": buf["resid_h"][:consumed].numpy().copy(),
-                       "gain": buf["gain_h"].numpy().copy()}
+                res = {"branch": buf["branch_h_np"][:consumed].copy(),
+                       "resid": buf["resid_h_np"][:consumed].copy(),
+                       "gain": buf["gain_h_np"].copy()}
             done += consumed
             if status & _lib.ST_RANK_CAP:
                 bs.grow(2 * bs.r_cap)
