@@ -447,11 +447,15 @@ def run_ours(args):
                               f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)"),
                        "sharding": (f"{S} contiguous streams per GPU of {B}, no collective" if cfg.streams > 1 else
                                     "single stream: one replica per GPU (rows are sequential; replicas only)")},
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
                          "traffic": ncu_traffic(args.config, args.dtype),
                          "algorithmic_flops_per_launch": flops_total / world,
                          "kernel_ms": kern_ms, "peak_source": peak_src,
+                         "note": ("bound by the fp64 tensor pipe (mma.sync DMMA; tcgen05 has no f64 kind); achieved "
+                                  "counts the reference's per-row op count (SURVEY.md 8(d)) over the branch log -- "
+                                  "the blocked algebra executes ~65% of it as MMAs, so frac can exceed the DMMA "
+                                  "pipe utilisation ncu reports (profiles/)"),
                          "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": mp.get("hbm_gbs"),
                                  "frac": hbm_gbs / mp["hbm_gbs"] if mp.get("hbm_gbs") else None,
                                  "algorithmic_bytes_per_launch": byt}},
