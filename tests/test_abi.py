@@ -70,6 +70,13 @@ def test_negative_fixed_eps_and_null_state(lib):
     assert "null" in lib.rgb_last_error().decode()
 
 
+def test_memcpy_helper_validates_without_a_device(lib):
+    assert lib.rgb_memcpy_async(None, None, 0, None) == _lib.OK
+    assert lib.rgb_memcpy_async(ctypes.c_void_p(8), None, 16, None) == _lib.E_INVALID
+    assert lib.rgb_memcpy_async(ctypes.c_void_p(8), ctypes.c_void_p(16), -1, None) == _lib.E_INVALID
+    assert "rgb_memcpy_async" in lib.rgb_last_error().decode()
+
+
 def test_product_has_no_oracle_dependency():
     pkg = os.path.join(ROOT, "paper_2106_11594_b200")
     for dirpath, _, files in os.walk(pkg):
