@@ -787,3 +787,22 @@ def test_runs_are_bitwise_deterministic(cfg, r_cap, streams, n):
     assert np.array_equal(a["branch"], b["branch"]) and np.array_equal(a["rank"], b["rank"])
     assert np.array_equal(a["x"], b["x"])
     assert np.array_equal(a["solver"].gram_t.cpu().numpy(), b["solver"].gram_t.cpu().numpy())
+
+
+def test_cluster_kernel_more_streams_than_clusters():
+    """20 streams of m = 1024 on 16-CTA clusters (at most ~9 resident): each
+    cluster folds several streams in turn, its mbarrier phases and ring slots
+    carrying over from one stream to the next."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    B, n, m = 20, 100, 1024
+    rows, tg = _lowrank_streams(B, n, m, 30, 2, seed=77)
+    o = oracle.ingest(rows, tg, r_cap=64, nthreads=8)
+    bs = BatchedSolver(B, m, k=2, r_cap=64)
+    br = torch.zeros((B, n), dtype=torch.uint8, device="cuda")
+    bs.ingest(dev(rows), dev(tg), branch_log=br)
+    torch.cuda.synchronize()
+    assert np.array_equal(bs.rank.cpu().numpy(), o["rank"]) and (o["rank"] == 30).all()
+    assert np.array_equal(br.cpu().numpy(), o["branch"])
+    X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
+    assert max(relerr(X[b], XO[b]) for b in range(B)) <= 1e-10
