@@ -806,3 +806,16 @@ def test_cluster_kernel_more_streams_than_clusters():
     assert np.array_equal(br.cpu().numpy(), o["branch"])
     X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
     assert max(relerr(X[b], XO[b]) for b in range(B)) <= 1e-10
+
+
+def test_grid_kernel_several_streams_in_turn():
+    """The grid kernel folds up to four large streams one after the other in a
+    single cooperative launch (workspace and barrier epochs carry over)."""
+    B, n, m = 3, 120, 1536
+    rows, tg = _lowrank_streams(B, n, m, 70, 1, seed=78)
+    res = run_batched(rows, tg, r_cap=128)
+    o = oracle.ingest(rows, tg, r_cap=128, nthreads=8)
+    assert np.array_equal(res["rank"], o["rank"]) and (o["rank"] == 70).all()
+    assert np.array_equal(res["branch"], o["branch"])
+    X = oracle.solution(o)
+    assert max(relerr(res["x"][b], X[b]) for b in range(B)) <= 1e-10
