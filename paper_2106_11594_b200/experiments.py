@@ -62,22 +62,31 @@ class BenchPlan:
     seed: int = 0
 
     def __post_init__(self):
-        if self.experiment not in EXPERIMENTS:
-            raise ValueError(f"unknown experiment {self.experiment!r}")
-        if self.repetitions < 3:
-            raise ValueError("repetitions must be at least 3")
-        if len(self.grid) < 2:
-            raise ValueError("need at least two grid sizes")
-        swept = [self.swept_size(cell) for cell in self.grid]
-        if any(later <= earlier for earlier, later in zip(swept, swept[1:])):
-            raise ValueError("grid must be strictly increasing in the swept parameter")
-        for n, m, r in self.grid:
-            if not 1 <= r <= min(n, m):
-                raise ValueError(f"invalid grid cell {(n, m, r)}")
+        _validate(self)
 
     def swept_size(self, cell):
-        n, m, r = cell
-        return {"rect-fixed-n": m, "update-cost": r}.get(self.experiment, n)
+        """The grid coordinate an experiment varies: m, r, or n."""
+        return {"rect-fixed-n": cell[1], "update-cost": cell[2]}.get(self.experiment, cell[0])
+
+
+def _validate(plan):
+    """ValueError for a malformed plan (the reference's checks, bench.py:65-78)."""
+    problems = []
+    if plan.experiment not in EXPERIMENTS:
+        problems.append(f"experiment must be one of {EXPERIMENTS}, got {plan.experiment!r}")
+    elif plan.repetitions < 3:
+        problems.append(f"at least 3 repetitions are required, got {plan.repetitions}")
+    elif len(plan.grid) < 2:
+        problems.append("a plan needs two or more grid cells")
+    else:
+        sizes = np.array([plan.swept_size(c) for c in plan.grid])
+        if (np.diff(sizes) <= 0).any():
+            problems.append(f"swept sizes must increase strictly, got {sizes.tolist()}")
+        bad = [c for c in plan.grid if not (1 <= c[2] <= min(c[0], c[1]))]
+        if bad:
+            problems.append(f"cells need 1 <= r <= min(n, m): {bad}")
+    if problems:
+        raise ValueError(problems[0])
 
 
 def make_plan(experiment, sizes, *, fixed_n=100, fixed_r=100, fixed_m=2000, repetitions=5,
@@ -91,7 +100,7 @@ def make_plan(experiment, sizes, *, fixed_n=100, fixed_r=100, fixed_m=2000, repe
         "update-cost": lambda v: (v, fixed_m, v),
     }
     if experiment not in cells:
-        raise ValueError(f"unknown experiment {experiment!r}")
+        raise ValueError(f"experiment must be one of {EXPERIMENTS}, got {experiment!r}")
     grid = tuple(cells[experiment](v) for v in sizes)
     return BenchPlan(experiment, grid, repetitions=repetitions, variant=variant, scalar=scalar, seed=seed)
 
@@ -101,7 +110,7 @@ def fit_loglog(sizes, seconds):
     x = np.log(np.asarray(sizes, dtype=np.float64))
     t = np.log(np.asarray(seconds, dtype=np.float64))
     if len(x) < 2:
-        raise ValueError("need at least two points to fit")
+        raise ValueError("a power-law fit needs two or more points")
     slope, icpt = np.polyfit(x, t, 1)
     resid = t - (slope * x + icpt)
     ss_res = float(resid @ resid)
@@ -112,9 +121,9 @@ def fit_loglog(sizes, seconds):
 
 def fit_tail(sizes, seconds):
     """Fit over the largest half of the grid, at least two points (bench.py:121-125)."""
-    idx = np.argsort(sizes)
-    keep = idx[len(idx) // 2:] if len(idx) > 3 else idx[-2:]
-    return fit_loglog([sizes[i] for i in keep], [seconds[i] for i in keep])
+    order = np.argsort(sizes)
+    tail = order[len(order) // 2:] if len(order) > 3 else order[-2:]
+    return fit_loglog(np.asarray(sizes)[tail], np.asarray(seconds)[tail])
 
 
 def _sync():
@@ -132,32 +141,32 @@ def _cell_seed(plan, index, stream):
 
 def solve_inputs(plan, index, cell):
     """(A, y) of a solve cell: seeded exactly as the reference's (bench.py:176-178)."""
-    n, m, r = cell
-    A = random_standardized(n, m, r, _cell_seed(plan, index, 0))
-    y = np.random.default_rng(_cell_seed(plan, index, 1)).standard_normal(n)
-    return A, y
+    rows, cols, rank = cell
+    matrix = random_standardized(rows, cols, rank, _cell_seed(plan, index, 0))
+    targets = np.random.default_rng(_cell_seed(plan, index, 1)).standard_normal(rows)
+    return matrix, targets
 
 
 def update_inputs(plan, index, cell, block=32):
     """(basis rows, their targets, dependent probes, probe targets) of an
     update-cost cell, drawn in the reference's order (bench.py:189-201)."""
-    r, m, _ = cell
-    rng = np.random.default_rng(_cell_seed(plan, index, 0))
-    basis_rows = rng.standard_normal((r, m))
-    basis_y = rng.standard_normal(r)
-    probes = rng.standard_normal((block, r)) @ basis_rows
-    return basis_rows, basis_y, probes, rng.standard_normal(block)
+    rank, width = cell[0], cell[1]
+    gen = np.random.default_rng(_cell_seed(plan, index, 0))
+    basis = gen.standard_normal((rank, width))
+    basis_y = gen.standard_normal(rank)
+    probes = gen.standard_normal((block, rank)) @ basis
+    return basis, basis_y, probes, gen.standard_normal(block)
 
 
 def _solve_cell(plan, index, cell):
     from .solver import solve_batch
 
-    A, y = solve_inputs(plan, index, cell)
+    matrix, targets = solve_inputs(plan, index, cell)
 
     def timed():
         _sync()
         t0 = time.perf_counter()
-        solve_batch(A, y, variant=plan.variant, scalar=plan.scalar)
+        solve_batch(matrix, targets, variant=plan.variant, scalar=plan.scalar)
         _sync()
         return time.perf_counter() - t0
 
@@ -168,23 +177,23 @@ def _update_cell(plan, index, cell):
     """Per-update cost of dependent rows at rank r, width m (bench.py:187-211)."""
     from .solver import RecursiveSolver
 
-    r, m, _ = cell
+    rank, width = cell[0], cell[1]
     block = 32  # probes per timed quantum
-    basis_rows, basis_y, probes, targets = update_inputs(plan, index, cell, block)
-    solver = RecursiveSolver(m, variant=plan.variant, scalar=plan.scalar)
-    solver.ingest(basis_rows, basis_y)
-    if solver.rank != r:
-        raise RuntimeError(f"prefix did not reach rank {r}")
+    basis, basis_y, probes, probe_y = update_inputs(plan, index, cell, block)
+    s = RecursiveSolver(width, variant=plan.variant, scalar=plan.scalar)
+    s.ingest(basis, basis_y)
+    if s.rank != rank:
+        raise RuntimeError(f"the basis prefix reached rank {s.rank}, expected {rank}")
 
     def timed():
         _sync()
         t0 = time.perf_counter()
-        solver.ingest(probes, targets)
+        s.ingest(probes, probe_y)
         _sync()
-        per_update = (time.perf_counter() - t0) / block
-        if solver.rank != r:
-            raise RuntimeError("probe updates unexpectedly grew the rank")
-        return per_update
+        dt = time.perf_counter() - t0
+        if s.rank != rank:
+            raise RuntimeError("a dependent probe changed the rank")
+        return dt / block
 
     return timed
 
@@ -195,25 +204,24 @@ def run_plan(plan, progress=None):
     One discarded warm-up per cell, then repetitions interleaved round-robin
     across cells so that drift hits every cell alike.
     """
-    make = _update_cell if plan.experiment == "update-cost" else _solve_cell
-    timers = [make(plan, i, cell) for i, cell in enumerate(plan.grid)]
-    for timer in timers:
-        timer()
-    times = [[] for _ in plan.grid]
-    for _ in range(plan.repetitions):
-        for slot, timer in enumerate(timers):
-            times[slot].append(timer())
-    samples, medians, swept = [], [], []
-    for slot, cell in enumerate(plan.grid):
-        samples.extend(BenchSample(plan.experiment, *cell, rep, sec) for rep, sec in enumerate(times[slot]))
-        medians.append(float(np.median(times[slot])))
-        swept.append(plan.swept_size(cell))
-        if medians[-1] < MIN_TIMED_SECONDS:
-            warnings.warn(f"cell {cell} of {plan.experiment} ran in {medians[-1]:.2e}s; "
+    build = _update_cell if plan.experiment == "update-cost" else _solve_cell
+    cells = list(plan.grid)
+    runners = [build(plan, i, cell) for i, cell in enumerate(cells)]
+    for run in runners:  # warm-up, discarded
+        run()
+    # rounds[rep][i]: repetition rep of cell i
+    rounds = [[run() for run in runners] for _ in range(plan.repetitions)]
+    per_cell = np.array(rounds).T
+    samples = [BenchSample(plan.experiment, *cell, rep, float(sec))
+               for cell, row in zip(cells, per_cell) for rep, sec in enumerate(row)]
+    medians = np.median(per_cell, axis=1)
+    for cell, med in zip(cells, medians):
+        if med < MIN_TIMED_SECONDS:
+            warnings.warn(f"cell {cell} of {plan.experiment} ran in {med:.2e}s; "
                           "timer resolution may dominate", stacklevel=2)
         if progress is not None:
-            progress(cell, medians[-1])
-    return samples, fit_tail(swept, medians)
+            progress(cell, float(med))
+    return samples, fit_tail([plan.swept_size(c) for c in cells], medians.tolist())
 
 
 def write_csv(samples, path):
@@ -221,5 +229,4 @@ def write_csv(samples, path):
     with open(path, "w", newline="", encoding="ascii") as fh:
         out = csv.writer(fh)
         out.writerow(["experiment", "n", "m", "r", "rep", "seconds"])
-        for s in samples:
-            out.writerow([s.experiment, s.n, s.m, s.r, s.rep, f"{s.seconds:.17g}"])
+        out.writerows([b.experiment, b.n, b.m, b.r, b.rep, f"{b.seconds:.17g}"] for b in samples)
