@@ -819,3 +819,26 @@ def test_grid_kernel_several_streams_in_turn():
     assert np.array_equal(res["branch"], o["branch"])
     X = oracle.solution(o)
     assert max(relerr(res["x"][b], X[b]) for b in range(B)) <= 1e-10
+
+
+@pytest.mark.parametrize("cfg,r_cap,variant", [("c5", 16, "general"), ("c3", 32, "orthonormal")])
+def test_batched_covariance_matches_closed_form(cfg, r_cap, variant):
+    """BatchedSolver.covariance (rgb_covariance): V = C~^T P^-1 C~ = A+ A+^T
+    (tracking.py:88-119, the identity of test_tracking.py:188-198) from the
+    device factors, against the oracle's factors and against A+ A+^T of the
+    device's own coords log."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch(cfg, list(range(12)), n=200)
+    res = run_batched(rows, tg, r_cap=r_cap, variant=variant)
+    o = oracle.ingest(rows, tg, r_cap=r_cap, variant=variant, nthreads=8)
+    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0))
+    bs = res["solver"]
+    V = bs.covariance().cpu().numpy()
+    pinv = bs.pinv(dev(res["coords"])).cpu().numpy()
+    for b in np.nonzero(ok)[0]:
+        r = int(o["rank"][b])
+        D = (o["C"] if variant == "orthonormal" else o["D"])[b, :r]
+        Vo = D.T @ o["P"][b, :r, :r] @ D
+        assert relerr(V[b], Vo) <= 1e-9
+        assert relerr(V[b], pinv[b] @ pinv[b].T) <= 1e-9
