@@ -87,3 +87,21 @@ def build_peak_probe(force=False):
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stderr[-4000:])
     return PEAK_LIB
+
+
+DEMO_SRC = os.path.join(ROOT, "examples", "rgb_demo.c")
+DEMO_BIN = os.path.join(ROOT, "examples", "rgb_demo")
+
+
+def build_demo(force=False):
+    """The plain-C consumer of the ABI (examples/rgb_demo.c), linked against librgb.so."""
+    if not force and os.path.exists(DEMO_BIN) and os.path.getmtime(DEMO_BIN) > os.path.getmtime(DEMO_SRC):
+        return DEMO_BIN
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    cmd = ["gcc", "-O2", "-o", DEMO_BIN, DEMO_SRC, "-I" + os.path.join(ROOT, "include"),
+           "-I" + os.path.join(cuda, "include"), "-L" + HERE, "-lrgb", "-L" + os.path.join(cuda, "lib64"),
+           "-lcudart", "-lm", "-Wl,-rpath,$ORIGIN/../paper_2106_11594_b200"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("demo build failed:\n" + res.stderr[-2000:])
+    return DEMO_BIN

@@ -114,3 +114,10 @@ def test_constructor_validation_without_device():
         p.RecursiveSolver(2, scalar="f64")
     with pytest.raises(p.CapabilityError):
         p.RecursiveSolver(2, variant="orthonormal", scalar=p.RATIONAL)
+
+
+def test_plain_c_consumer_builds():
+    """examples/rgb_demo.c uses only include/rgb.h and the CUDA runtime (no torch)."""
+    from paper_2106_11594_b200 import _build
+
+    assert os.path.exists(_build.build_demo(force=True))

@@ -842,3 +842,14 @@ def test_batched_covariance_matches_closed_form(cfg, r_cap, variant):
         Vo = D.T @ o["P"][b, :r, :r] @ D
         assert relerr(V[b], Vo) <= 1e-9
         assert relerr(V[b], pinv[b] @ pinv[b].T) <= 1e-9
+
+
+def test_plain_c_consumer_runs():
+    """The ABI from C: rank 3 of a 12 x 6 integer system, consistent x."""
+    import subprocess
+
+    from paper_2106_11594_b200 import _build
+
+    out = subprocess.run([_build.build_demo()], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "rank 3 status 0" in out.stdout
