@@ -1,9 +1,14 @@
 // rgb_abi.cu -- extern "C" entry points of librgb.so (declared in include/rgb.h).
 //
 // Validation mirrors the reference's constructor and input checks
-// (solver.py:142-158, scalars.py:108-138) as return codes; dispatch picks the
-// tensor-core blocked kernel for the shapes it is specialised for and the
-// shape-generic kernel otherwise.  No host allocation, no hidden state.
+// (solver.py:142-158, scalars.py:108-138) as return codes.  Dispatch, first
+// match wins: the one-warp tensor-core kernel (m 64, r_cap 16, k <= 8), the
+// warp-group kernel (m 128 / r_cap 32, m 256 / r_cap 16), the cluster kernel
+// (r_cap 64, m <= 1 080) and the grid kernel (a few large streams, m <= 2 368,
+// r_cap <= 512) -- the last two for calls of 8+ rows -- and the shape-generic
+// kernel for everything else, for fp32 state and for per-row residual logs.
+// No host allocation, no hidden state (the grid kernel's workspace is
+// stream-ordered, cudaMallocAsync).
 #include <stdio.h>
 #include <string.h>
 

@@ -40,8 +40,11 @@
 //   P^-1   Pr[mt][nt][e] = P[8mt+p][8nt+2q+e]           registers (symmetric)
 //   W^T    Wt[nt][e]     = W[8nt+2q+e][c=p]             registers
 //
-// Specialised for the batched configuration m = 64, r_cap = 16, k = 8 (fp64,
-// general variant); every other shape runs on rgb_generic.cu.
+// Instantiated for the batched configuration m = 64, r_cap = 16, k <= 8
+// right-hand sides (unused RHS lanes masked), fp64 state, all three variants
+// (the orthogonal / orthonormal growth in its own instantiation), float64 or
+// float32 inputs; other shapes run on the warp-group, cluster, grid or
+// generic kernels.
 #include "rgb_mma.cuh"
 
 namespace rgb {

@@ -4,8 +4,8 @@
 // live in the caller's global buffers (L2 resident for the single-stream
 // configs), threads own strided columns j of C, C~, x; warps own rows i of
 // C~ and P^-1 for the reductions over m and r.  This kernel covers every
-// (m, r_cap, k, variant, dtype) the ABI accepts; the batched configurations
-// run on the specialised tensor-core kernel in rgb_blocked.cu.
+// (m, r_cap, k, variant, dtype) the ABI accepts; the shapes the tensor-core
+// kernels serve (rgb_blocked*.cu, rgb_cluster.cu, rgb_grid.cu) run there.
 //
 // Per row it restates RecursiveSolver.ingest (solver.py:276-319):
 //   coords  = C~ a                       solver.py:286

@@ -1,7 +1,8 @@
 // rgb_grid.cu -- one large stream on the whole GPU (sm_100a, fp64 tensor cores).
 //
-// For a single stream whose factors are too large for one SM (config 2:
-// m 1024, r 64; config 4: m 2048, r 512) the same 8-row tile algebra as
+// For a few single streams whose factors are too large for one SM (config 4:
+// m 2048, r 512; any m <= 2 368 with r_cap <= 512, columns past m and factor
+// rows past r_cap masked; config 2 runs on rgb_cluster.cu) the same 8-row tile algebra as
 // rgb_blocked.cu runs on NC cooperative CTAs (one per SM) separated by grid
 // barriers:
 //
