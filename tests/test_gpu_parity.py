@@ -388,13 +388,12 @@ def test_continuation_calls_match_one_shot(cfg, r_cap, splits):
         assert relerr(X[b], one["x"][b]) <= 1e-10
 
 
-@pytest.mark.parametrize("cfg,r_cap", [("c5", 16), ("c3", 32)])
+@pytest.mark.parametrize("cfg,r_cap", [("c5", 16), ("c3", 32), ("c2", 64), ("c4", 512)])
 def test_fixed_eps_policy_on_blocked_kernels(cfg, r_cap):
-    """EpsPolicy.fixed (solver.py:66-68) through the tensor-core kernels: a loose
-    threshold changes decisions exactly as in the oracle."""
-    from paper_2106_11594_b200 import workloads
-
-    rows, tg = workloads.host_batch(cfg, list(range(8)), n=128)
+    """EpsPolicy.fixed (solver.py:66-68) through the tensor-core kernels (one-warp,
+    warp-group, cluster, grid): a loose threshold changes decisions exactly as in
+    the oracle."""
+    rows, tg = _shape_rows(cfg, list(range(8)), 128 if cfg in ("c5", "c3") else 200)
     for eps in (1e-8, 1e-3):
         res = run_batched(rows, tg, r_cap=r_cap, eps=eps)
         o = oracle.ingest(rows, tg, r_cap=r_cap, eps=eps)
