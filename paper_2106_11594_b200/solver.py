@@ -251,7 +251,18 @@ class RecursiveSolver:
             self._st_key = key
         return self._st
 
+    # rows staged per device call: bounds the pinned and device staging buffers
+    # (a continuation call is equivalent to one long call)
+    _CHUNK_ROWS = 8192
+
     def _run(self, A, y, want_report):
+        n = A.shape[0]
+        res = {}
+        for s0 in range(0, n, self._CHUNK_ROWS):
+            res = self._run_block(A[s0:s0 + self._CHUNK_ROWS], y[s0:s0 + self._CHUNK_ROWS], want_report)
+        return res
+
+    def _run_block(self, A, y, want_report):
         torch = self._torch
         bs = self._bs
         lib = bs.lib
