@@ -21,6 +21,24 @@
 
 namespace rgb {
 namespace blk {
+// phase timing (debug builds only: -DRGB_WG_PROBE): clock64 cycles per phase,
+// summed over warp 0 of every CTA, read back with rgb_wg_probe()
+// (scripts/probe_wg.py)
+#ifdef RGB_WG_PROBE
+__device__ unsigned long long g_wprobe[16];
+#define WPROBE(i)                                                 \
+  do {                                                            \
+    if ((threadIdx.x & 31) == 0 && (threadIdx.x >> 5) == 0) {     \
+      const long long now_ = clock64();                           \
+      atomicAdd(&g_wprobe[i], (unsigned long long)(now_ - wp_t)); \
+      wp_t = now_;                                                \
+    }                                                             \
+  } while (0)
+#else
+#define WPROBE(i) \
+  do {            \
+  } while (0)
+#endif
 
 template <int R, int WG, typename TI>
 struct GroupSmem {
@@ -52,6 +70,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
   const int k = cfg.k;
   const int j0 = 32 * w;
 
+#ifdef RGB_WG_PROBE
+  long long wp_t = clock64();
+#endif
   for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
     int status = st.status[b];
     if (status) continue;  // uniform across the block
@@ -129,6 +150,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 
     // projection of one tile and the rank test (solver.py:286-296)
     auto front = [&](int64_t tile, int s, int row_start, Front& F) {
+      WPROBE(0);
       const TI* As = &S.At[w][s][0][lane][0];
       F.t0 = tile * TT;
       F.tv = (int)((T - F.t0) < TT ? (T - F.t0) : TT);
@@ -172,7 +194,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         *reinterpret_cast<double2*>(&S.Gp[w][nt][lane][0]) = make_double2(g[nt][0] + g2[nt][0], g[nt][1] + g2[nt][1]);
       *reinterpret_cast<double2*>(&S.red[0][w][lane][0]) = make_double2(asq, 0.0);
       *reinterpret_cast<double2*>(&S.red[2][w][lane][0]) = make_double2(y0[0], y0[1]);
+      WPROBE(1);
       __syncthreads();
+      WPROBE(2);
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) {
         double2 sum = make_double2(0.0, 0.0);
@@ -220,7 +244,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       rsq += __shfl_xor_sync(FULL, rsq, 1);
       rsq += __shfl_xor_sync(FULL, rsq, 2);
       S.red[1][w][lane][0] = rsq;
+      WPROBE(3);
       __syncthreads();
+      WPROBE(4);
       rsq = 0.0;
 #pragma unroll
       for (int u = 0; u < WG; ++u) rsq += S.red[1][u][lane][0];
@@ -238,6 +264,7 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 
     // blocked Sherman-Morrison over the dependent rows [rs, te) (solver.py:297-304)
     auto scan = [&](const Front& F, int rs, int te) {
+      WPROBE(6);
       const bool inb = p >= rs && p < te;
       double gm[IT][2];
 #pragma unroll
@@ -262,7 +289,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
       }
       *reinterpret_cast<double2*>(&S.Sp[w][lane][0]) = make_double2(sp[0], sp[1]);
       *reinterpret_cast<double2*>(&S.red[2][w][lane][0]) = make_double2(gw[0], gw[1]);
+      WPROBE(7);
       __syncthreads();
+      WPROBE(8);
       double mi[2] = {0.0, 0.0}, gws[2] = {0.0, 0.0};
 #pragma unroll
       for (int u = 0; u < WG; ++u) {
@@ -315,7 +344,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         mma(yt, u[1], ev[1]);
         *reinterpret_cast<double2*>(&S.Yb[w][lane][0]) = make_double2(yt[0], yt[1]);
       }
+      WPROBE(9);
       __syncthreads();
+      WPROBE(10);
       if (own) {
         // E dy0 (every RHS), then P[own rows] -= Y^T D^-1 Y and W[own] += ...
         double dh[2] = {0.0, 0.0};
@@ -636,7 +667,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
         break;
       }
       consumed = F.t0 + F.tv;
+      WPROBE(12);
       __syncthreads();  // every warp is done with stage s before it is refilled
+      WPROBE(13);
       prefetch(tile + 2, s);
       cp_wait<1>();
       __syncwarp();
@@ -742,3 +775,14 @@ int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, in
 }
 
 }  // namespace rgb
+
+#ifdef RGB_WG_PROBE
+extern "C" int rgb_wg_probe(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rgb::blk::g_wprobe, sizeof(rgb::blk::g_wprobe));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(rgb::blk::g_wprobe, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -1,5 +1,9 @@
-"""Per-phase cycles of the warp-group kernel (probe build in scratch/wgp): warp 0
-of every CTA, summed; printed per tile-visit."""
+"""Per-phase cycles of the warp-group kernel: warp 0 of every CTA, summed,
+printed per tile.  Needs the probe build:
+
+    nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -shared -Xcompiler -fPIC \
+        -DRGB_WG_PROBE -Iinclude -o scratch/wgp/librgb.so paper_2106_11594_b200/csrc/*.cu
+"""
 import ctypes
 import os
 import sys
