@@ -719,15 +719,17 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
-// Single large streams of any width up to 148 x 16 columns and capacity up to
-// 512: the smallest instantiated R >= r_cap.  (Small problems stay on the
+// Single large streams of any width up to 148 x 16 columns with capacity up
+// to 512, or up to 148 x 32 columns with capacity up to 256: the smallest
+// instantiated R >= r_cap.  (Small problems stay on the
 // generic kernel: a grid step costs a few microseconds of barriers.)
 bool grid_supports(const rgb_config& cfg) {
   const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
                       (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
   if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
   if (cfg.num_streams > 4) return false;  // a handful of large streams, one after the other
-  if (cfg.r_cap > 512 || cfg.m > 148 * 16) return false;
+  if (cfg.r_cap > 512 || cfg.m > 148 * 32) return false;
+  if (cfg.m > 148 * 16 && cfg.r_cap > 256) return false;  // 32-column slices: R <= 256 fits shared memory
   return (int64_t)cfg.m * cfg.r_cap >= 32768;
 }
 
@@ -735,6 +737,13 @@ template <typename TI>
 static int launch_grid_r(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                          const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                          cudaStream_t stream, int num_sms) {
+  if (cfg.m > 148 * 16) {  // wide streams: 32 columns per CTA
+    if (cfg.r_cap <= 64)
+      return launch_grid_t<64, 32, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    if (cfg.r_cap <= 128)
+      return launch_grid_t<128, 32, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+    return launch_grid_t<256, 32, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  }
   if (cfg.r_cap <= 64 && cfg.m <= 148 * 8)
     return launch_grid_t<64, 8, TI>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   if (cfg.r_cap <= 64)

@@ -708,10 +708,12 @@ def test_cluster_kernel_nonfinite_and_rank_cap():
 
 @pytest.mark.parametrize("m,r_cap,r,n,tol", [(2000, 512, 100, 260, 1e-9), (700, 128, 90, 200, 1e-9),
                                              (2048, 64, 20, 300, 1e-9), (300, 256, 150, 170, 1e-9),
-                                             (512, 512, 512, 512, 1e-6)])
+                                             (512, 512, 512, 512, 1e-6), (4000, 256, 120, 200, 1e-9),
+                                             (3000, 64, 40, 150, 1e-9), (4736, 128, 70, 120, 1e-9)])
 def test_grid_kernel_any_width_and_capacity(m, r_cap, r, n, tol):
-    """The grid kernel serves any single large stream (m up to 2368, r_cap up
-    to 512; columns past m and factor rows past r_cap masked): branches, rank,
+    """The grid kernel serves any single large stream (m up to 2368 with r_cap
+    up to 512, or up to 4736 with r_cap up to 256; columns past m and factor
+    rows past r_cap masked): branches, rank,
     x and the stored factors against the oracle, including a full-rank square
     system that fills the capacity exactly."""
     rows, tg = _lowrank_streams(1, n, m, r, 2, seed=m + r)
