@@ -730,8 +730,9 @@ __global__ void __launch_bounds__(WG * 32, (WG <= 4 ? 3 : 1)) blocked_wg_kernel(
 
 }  // namespace blk
 
-// Instantiations: (r_cap, warps) with m = 32 * warps -- config 3 (m 128,
-// r_cap 32) and config 1 (m 256, r_cap 16, one stream: 8 warps share its work).
+// Instantiations: (r_cap, warps) with m = 32 * warps, r_cap 16 or 32 -- config 3
+// (m 128, r_cap 32), config 1 (m 256, r_cap 16, one stream: 8 warps share its
+// work), and m 128 / r_cap 16, m 256 / r_cap 32.
 template <int R, int WG, typename TI>
 static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                      const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
@@ -758,7 +759,7 @@ bool blocked_wg_supports(const rgb_config& cfg) {
   const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
                       (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
   if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
-  return (cfg.m == 128 && cfg.r_cap == 32) || (cfg.m == 256 && cfg.r_cap == 16);
+  return (cfg.m == 128 || cfg.m == 256) && (cfg.r_cap == 16 || cfg.r_cap == 32);
 }
 
 int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
@@ -771,6 +772,12 @@ int launch_blocked_wg(const rgb_config& cfg, rgb_state& st, const void* rows, in
   if (cfg.m == 256 && cfg.r_cap == 16)
     return f32in ? launch_wg<16, 8, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
                  : launch_wg<16, 8, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.m == 128 && cfg.r_cap == 16)
+    return f32in ? launch_wg<16, 4, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_wg<16, 4, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
+  if (cfg.m == 256 && cfg.r_cap == 32)
+    return f32in ? launch_wg<32, 8, float>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms)
+                 : launch_wg<32, 8, double>(cfg, st, rows, rows_stride, targets, tg_stride, T, logs, stream, num_sms);
   return RGB_E_UNSUPPORTED;
 }
 

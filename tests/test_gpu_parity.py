@@ -865,7 +865,8 @@ def test_random_shapes_against_oracle(seed):
 
     rng = np.random.default_rng(1000 + seed)
     shapes = [(64, 16, 8), (64, 16, 3), (128, 32, 1), (256, 16, 2), (512, 64, 4), (1024, 64, 1),
-              (700, 128, 2), (48, 24, 5), (96, 8, 1), (2000, 256, 1)]
+              (700, 128, 2), (48, 24, 5), (96, 8, 1), (2000, 256, 1), (128, 16, 2), (256, 32, 1),
+              (4000, 128, 1)]
     for _ in range(3):
         m, r_cap, k = shapes[int(rng.integers(len(shapes)))]
         variant = ["general", "orthogonal", "orthonormal"][int(rng.integers(3))]
@@ -894,3 +895,25 @@ def test_random_shapes_against_oracle(seed):
         X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
         for b in np.nonzero(ok)[0]:
             assert relerr(X[b], XO[b]) <= 1e-9, case
+
+
+@pytest.mark.parametrize("m,r_cap", [(128, 16), (256, 32)])
+@pytest.mark.parametrize("variant", ["general", "orthonormal"])
+def test_warp_group_kernel_other_instantiations(m, r_cap, variant):
+    """Warp-group kernel at m 128 / r_cap 16 (4 warps, two own a P block) and
+    m 256 / r_cap 32 (8 warps): many streams, ranks up to the capacity."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    B, n = 24, 200
+    rng = np.random.default_rng(m + r_cap)
+    rs = rng.integers(1, r_cap + 1, size=B)
+    rows = np.stack([_lowrank_streams(1, n, m, int(r), 1, seed=int(b))[0][0] for b, r in enumerate(rs)])
+    tg = rng.standard_normal((B, n, 1))
+    o = oracle.ingest(rows, tg, r_cap=r_cap, variant=variant, nthreads=8)
+    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (o["rank"] != rs))
+    assert ok.sum() >= B - 2
+    res = run_batched(rows, tg, r_cap=r_cap, variant=variant)
+    assert np.array_equal(res["branch"][ok], o["branch"][ok])
+    assert np.array_equal(res["rank"][ok], o["rank"][ok])
+    X = oracle.solution(o)
+    assert max(relerr(res["x"][b], X[b]) for b in np.nonzero(ok)[0]) <= 1e-10
