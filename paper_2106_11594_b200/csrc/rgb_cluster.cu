@@ -199,9 +199,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
     if (status) continue;  // uniform across the cluster
     int r = st.rank[b];
     const int64_t nobs0 = st.nobs[b];
-    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)R * M;
-    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)R * M;
-    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)R * R;
+    const int rc = cfg.r_cap;  // stored capacity (<= R): global row stride; rows past it are zero
+    double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)rc * M;
+    double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)rc * M;
+    double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)rc * rc;
     double* Xg = reinterpret_cast<double*>(st.x) + b * (int64_t)k * M;
     const TI* Rb = rows + b * rstride;
     const TI* Yb = tgts + b * tstride;
@@ -217,15 +218,16 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         const int i = 8 * nt + (l >> 2), col = c0 + 4 * kt + (l & 3);
         double v = 0.0;
         if (col < M) {
-          if (i < R) v = Dg[(int64_t)i * M + col];
-          else if (i - R < k) v = Xg[(int64_t)(i - R) * M + col];
+          if (i < rc) v = Dg[(int64_t)i * M + col];
+          else if (i >= R && i - R < k) v = Xg[(int64_t)(i - R) * M + col];
         }
         C.Ds[nt][kt][l] = v;
       }
       for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
         const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
         const int col = c0 + 8 * nt + (l >> 2);
-        C.Cs[kt][nt][l] = col < M ? -Cg[(int64_t)(4 * kt + (l & 3)) * M + col] : 0.0;
+        const int i = 4 * kt + (l & 3);
+        C.Cs[kt][nt][l] = (col < M && i < rc) ? -Cg[(int64_t)i * M + col] : 0.0;
       }
       auto prefetch = [&](int64_t pan, int s) {
         if (pan < npan) {
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           proj += 1;
           PROBE(6);
           if (tstar >= tv) break;
-          if (((badm >> tstar) & 1u) || r >= R) {
+          if (((badm >> tstar) & 1u) || r >= rc) {
             status |= ((badm >> tstar) & 1u) ? RGB_ST_NONFINITE : RGB_ST_RANK_CAP;
             stopped = true;
             consumed = t0 + tstar;
@@ -434,12 +436,14 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
         const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
         const int col = c0 + 4 * kt + (l & 3);
-        if (col < M) Dg[(int64_t)(8 * nt + (l >> 2)) * M + col] = C.Ds[nt][kt][l];
+        const int i = 8 * nt + (l >> 2);
+        if (col < M && i < rc) Dg[(int64_t)i * M + col] = C.Ds[nt][kt][l];
       }
       for (int e = tid; e < (R / 4) * (CW / 8) * 32; e += NT) {
         const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
         const int col = c0 + 8 * nt + (l >> 2);
-        if (col < M) Cg[(int64_t)(4 * kt + (l & 3)) * M + col] = -C.Cs[kt][nt][l];
+        const int i = 4 * kt + (l & 3);
+        if (col < M && i < rc) Cg[(int64_t)i * M + col] = -C.Cs[kt][nt][l];
       }
       cluster_sync_all();  // home has folded every projection: W is final
       {
@@ -462,7 +466,10 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
     } else {
       // ======================= home CTA: P^-1 and W ===================================
       auto& H = S.u.home;
-      for (int e = tid; e < R * R; e += NT) H.Ps[e / R][e % R] = Pg[e];
+      for (int e = tid; e < R * R; e += NT) {
+        const int i = e / R, i2 = e % R;
+        H.Ps[i][i2] = (i < rc && i2 < rc) ? Pg[(int64_t)i * rc + i2] : 0.0;
+      }
       for (int e = tid; e < R * 8; e += NT) H.Wb[e >> 3][e & 7] = 0.0;
       auto prefetch = [&](int64_t pan, int s) {
         if (pan < npan) {
@@ -604,7 +611,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           const int64_t row = b * T + t0 + base + tid;
           if (blog) blog[row] = 0;
           if (clog)
-            for (int i = 0; i < R; ++i) clog[row * R + i] = Gs[base + tid][i];
+            for (int i = 0; i < rc; ++i) clog[row * rc + i] = Gs[base + tid][i];
         }
         __syncthreads();
         PROBE(13);
@@ -652,7 +659,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           __syncthreads();
           for (int base = (row_start & ~7); base < tstar; base += 8) dep_block(s, Gs, base, row_start, tstar, t0);
           bool done = tstar >= tv;
-          if (!done && (((badm >> tstar) & 1u) || r >= R)) {
+          if (!done && (((badm >> tstar) & 1u) || r >= rc)) {
             status |= ((badm >> tstar) & 1u) ? RGB_ST_NONFINITE : RGB_ST_RANK_CAP;
             stopped = true;
             consumed = t0 + tstar;
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
                 const int64_t row = b * T + t0 + ts;
                 if (blog) blog[row] = 1;
                 if (clog)
-                  for (int i = 0; i < R; ++i) clog[row * R + i] = (i == r) ? 1.0 : 0.0;
+                  for (int i = 0; i < rc; ++i) clog[row * rc + i] = (i == r) ? 1.0 : 0.0;
               }
             } else {
               const double resc = (cfg.variant == RGB_ORTHONORMAL) ? 1.0 / sqrt(rsq_ts) : cfg.alpha;
@@ -702,7 +709,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
                 const int64_t row = b * T + t0 + ts;
                 if (blog) blog[row] = 1;
                 if (clog)
-                  for (int i = 0; i < R; ++i) clog[row * R + i] = i < r ? Gs[ts][i] : (i == r ? last : 0.0);
+                  for (int i = 0; i < rc; ++i) clog[row * rc + i] = i < r ? Gs[ts][i] : (i == r ? last : 0.0);
               }
             }
           }
@@ -718,7 +725,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         if (!stopped) consumed = t0 + tv;
       }
       blk::cp_wait<0>();
-      for (int e = tid; e < R * R; e += NT) Pg[e] = H.Ps[e / R][e % R];
+      for (int e = tid; e < rc * rc; e += NT) Pg[e] = H.Ps[e / rc][e % rc];
       cluster_sync_all();  // W final for the column CTAs
       cluster_sync_all();  // they have read it
     }
@@ -766,12 +773,14 @@ static int launch_cluster_t(const rgb_config& cfg, rgb_state& st, const void* ro
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
-// r_cap 64 and m up to 15 x 72 = 1 080 (a multiple of 4): 15 column CTAs at most
+// r_cap 16..64 (rows past r_cap masked) and m up to 15 x 72 = 1 080 (a
+// multiple of 4): 15 column CTAs at most
 bool cluster_supports(const rgb_config& cfg) {
   const bool var_ok = cfg.variant == RGB_GENERAL || cfg.variant == RGB_ORTHONORMAL ||
                       (cfg.variant == RGB_ORTHOGONAL && cfg.alpha != 0.0);
   if (cfg.dtype != RGB_F64 || !var_ok || cfg.k < 1 || cfg.k > 8) return false;
-  return cfg.r_cap == 64 && cfg.m % 4 == 0 && cfg.m >= 128 && cfg.m <= (cls::MAXCL - 1) * 72;
+  return cfg.r_cap >= 16 && cfg.r_cap <= 64 && cfg.m % 4 == 0 && cfg.m >= 128 &&
+         cfg.m <= (cls::MAXCL - 1) * 72;
 }
 
 int launch_cluster(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,

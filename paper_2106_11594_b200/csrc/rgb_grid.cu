@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             const int64_t row = b * T + t0 + tid;
             if (blog) blog[row] = 0;
             if (clog)
-              for (int i = 0; i < R; ++i) clog[row * R + i] = S.Gs[tid][i];
+              for (int i = 0; i < rc; ++i) clog[row * rc + i] = S.Gs[tid][i];
           }
           __syncthreads();
         }
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             const int64_t row = b * T + t0 + ts;
             if (blog) blog[row] = 1;
             if (clog)
-              for (int i = 0; i < R; ++i) clog[row * R + i] = (i == r) ? 1.0 : 0.0;
+              for (int i = 0; i < rc; ++i) clog[row * rc + i] = (i == r) ? 1.0 : 0.0;
           }
           __syncthreads();
           r += 1;
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             const int64_t row = b * T + t0 + ts;
             if (blog) blog[row] = 1;
             if (clog)
-              for (int i = 0; i < R; ++i) clog[row * R + i] = i < r ? S.Gs[ts][i] : (i == r ? last : 0.0);
+              for (int i = 0; i < rc; ++i) clog[row * rc + i] = i < r ? S.Gs[ts][i] : (i == r ? last : 0.0);
           }
           __syncthreads();
           r += 1;

@@ -198,13 +198,79 @@ def _update_cell(plan, index, cell):
     return timed
 
 
-def run_plan(plan, progress=None):
+def _device_solve_cell(plan, index, cell):
+    """Device time (CUDA events) of a solve from scratch on inputs already in
+    HBM: the state reset and the ingest kernel(s), without the host round trip."""
+    import torch
+
+    from .batched import BatchedSolver
+
+    matrix, targets = solve_inputs(plan, index, cell)
+    n, m, r = cell
+    rows = torch.as_tensor(matrix[None], device="cuda")
+    tg = torch.as_tensor(targets[None, :, None], device="cuda")
+    # the capacity the drop-in solver reaches for a rank-r stream (it doubles from 32)
+    cap = min(m, 1 << max(5, (r - 1).bit_length()))
+    bs = BatchedSolver(1, m, k=1, r_cap=cap, variant=plan.variant)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed():
+        bs.reset()
+        e0.record()
+        bs.ingest(rows, tg)
+        e1.record()
+        e1.synchronize()
+        if int(bs.status[0]) != 0:
+            raise RuntimeError(f"cell {cell}: device status {int(bs.status[0])}")
+        return e0.elapsed_time(e1) * 1e-3
+
+    return timed
+
+
+def _device_update_cell(plan, index, cell):
+    """Device time per dependent update: a block of probes folded into a
+    rank-r state (inputs in HBM)."""
+    import torch
+
+    from .batched import BatchedSolver
+
+    rank, width = cell[0], cell[1]
+    block = 32
+    basis, basis_y, probes, probe_y = update_inputs(plan, index, cell, block)
+    cap = 1 << max(3, (rank - 1).bit_length())
+    bs = BatchedSolver(1, width, k=1, r_cap=cap, variant=plan.variant)
+    bs.ingest(torch.as_tensor(basis[None], device="cuda"), torch.as_tensor(basis_y[None, :, None], device="cuda"))
+    if int(bs.rank[0]) != rank:
+        raise RuntimeError(f"the basis prefix reached rank {int(bs.rank[0])}, expected {rank}")
+    rows = torch.as_tensor(probes[None], device="cuda")
+    tg = torch.as_tensor(probe_y[None, :, None], device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed():
+        e0.record()
+        bs.ingest(rows, tg)
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1) * 1e-3 / block
+
+    return timed
+
+
+def run_plan(plan, progress=None, clock="wall"):
     """Run a plan: (samples, fit over per-cell medians) (bench.py:128-163).
 
     One discarded warm-up per cell, then repetitions interleaved round-robin
-    across cells so that drift hits every cell alike.
+    across cells so that drift hits every cell alike.  clock="wall" times the
+    drop-in call as the reference does (host arrays in, host results out);
+    clock="device" times the device work alone with CUDA events on inputs
+    already in HBM (the B200-side scaling of the same cells).
     """
-    build = _update_cell if plan.experiment == "update-cost" else _solve_cell
+    if clock not in ("wall", "device"):
+        raise ValueError(f"clock must be 'wall' or 'device', got {clock!r}")
+    if clock == "device":
+        build = _device_update_cell if plan.experiment == "update-cost" else _device_solve_cell
+    else:
+        build = _update_cell if plan.experiment == "update-cost" else _solve_cell
     cells = list(plan.grid)
     runners = [build(plan, i, cell) for i, cell in enumerate(cells)]
     for run in runners:  # warm-up, discarded

@@ -18,11 +18,12 @@ plans = {
     "update-cost": ex.make_plan("update-cost", [50, 100, 200, 400], fixed_m=2000, repetitions=5, seed=17),
 }
 res = {}
-for name, plan in plans.items():
+for (name, plan), clock in [(kv, c) for c in ("wall", "device") for kv in plans.items()]:
     t0 = time.perf_counter()
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
-        samples, fit = ex.run_plan(plan)
+        samples, fit = ex.run_plan(plan, clock=clock)
+    name = f"{name}_{clock}"
     ex.write_csv(samples, os.path.join(out_dir, f"scaling_{name}.csv"))
     med = {}
     for s in samples:

@@ -706,6 +706,31 @@ def test_cluster_kernel_nonfinite_and_rank_cap():
     assert relerr(bs.solution.cpu().numpy()[0], oracle.solution(o)[0]) <= 1e-10
 
 
+@pytest.mark.parametrize("m,r_cap,r,n", [(512, 32, 30, 260), (256, 48, 40, 150), (1024, 16, 12, 120),
+                                         (2048, 48, 40, 150), (3000, 40, 33, 120)])
+def test_cluster_and_grid_kernels_capacity_below_template(m, r_cap, r, n):
+    """A stored capacity below the kernel's template rank (cluster R = 64, grid
+    R = 64 for r_cap <= 64): the factors, P and the coords log use the r_cap
+    stride with the padding rows masked -- branches, rank, x, the factors and
+    the coords log against the oracle, then a stream that outgrows r_cap
+    freezes with RGB_ST_RANK_CAP at rank r_cap."""
+    rows, tg = _lowrank_streams(2, n, m, r, 2, seed=m + r_cap)
+    res = run_batched(rows, tg, r_cap=r_cap)
+    o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=2)
+    assert (o["rank"] == r).all() and (o["status"] == 0).all()
+    assert np.array_equal(res["rank"], o["rank"]) and (res["status"] == 0).all()
+    assert np.array_equal(res["branch"], o["branch"])
+    X = oracle.solution(o)
+    assert max(relerr(res["x"][b], X[b]) for b in range(2)) <= 1e-10
+    assert relerr(res["coords"], o["coords"]) <= 1e-9
+    bs = res["solver"]
+    assert relerr(bs.basis_t.cpu().numpy(), o["C"]) <= 1e-10
+    assert relerr(bs.gram_t.cpu().numpy(), o["P"]) <= 1e-8
+    over, otg = _lowrank_streams(1, 80, m, r_cap + 6, 1, seed=3)
+    res = run_batched(over, otg, r_cap=r_cap)
+    assert res["status"][0] & 1 and int(res["rank"][0]) == r_cap
+
+
 @pytest.mark.parametrize("m,r_cap,r,n,tol", [(2000, 512, 100, 260, 1e-9), (700, 128, 90, 200, 1e-9),
                                              (2048, 64, 20, 300, 1e-9), (300, 256, 150, 170, 1e-9),
                                              (512, 512, 512, 512, 1e-6), (4000, 256, 120, 200, 1e-9),
