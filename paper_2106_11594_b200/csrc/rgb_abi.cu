@@ -7,8 +7,9 @@
 // (r_cap 64, m <= 1 080) and the grid kernel (a few large streams, m <= 2 368,
 // r_cap <= 512) -- the last two for calls of 8+ rows -- and the shape-generic
 // kernel for everything else, for fp32 state and for per-row residual logs.
-// No host allocation, no hidden state (the grid kernel's workspace is
-// stream-ordered, cudaMallocAsync).
+// No host allocation and no per-call state (the grid kernel's workspace is
+// stream-ordered, from a library-owned device memory pool that is kept
+// between calls).
 #include <stdio.h>
 #include <string.h>
 

@@ -23,8 +23,14 @@
 // multi-SM scheme.  An independent row (solver.py:305-318) is applied by
 // every CTA to its own columns / row block, and the rest of its tile is
 // re-projected.  The workspace (partials, barrier counter) is allocated per
-// call with cudaMallocAsync on the caller's stream, so calls stay reentrant.
+// call, stream-ordered on the caller's stream, so calls stay reentrant; it
+// comes from a library-owned pool per device whose memory is kept between
+// calls (the default pool hands it back to the driver at every
+// synchronisation, and re-mapping cost 3.8 ms per call at m = 2048).
 #include <cooperative_groups.h>
+
+#include <cstdint>
+#include <mutex>
 
 #include "rgb_mma.cuh"
 
@@ -683,6 +689,31 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
 
 }  // namespace grd
 
+// Workspace pool of the current device: created once, never trimmed.
+static cudaMemPool_t workspace_pool() {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
+
 template <int R, int CW, typename TI>
 static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                          const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
@@ -703,7 +734,8 @@ static int launch_grid_t(const rgb_config& cfg, rgb_state& st, const void* rows,
   if (per_sm < 1) return RGB_E_UNSUPPORTED;
   const size_t wsb = grd::Ws<R, CW>::bytes(nc);
   void* ws = nullptr;
-  if (cudaMallocAsync(&ws, wsb, stream) != cudaSuccess) return RGB_E_CUDA;
+  cudaMemPool_t pool = workspace_pool();
+  if (!pool || cudaMallocFromPoolAsync(&ws, wsb, pool, stream) != cudaSuccess) return RGB_E_CUDA;
   cudaMemsetAsync(ws, 0, 256, stream);
   double* wsd = reinterpret_cast<double*>(ws);
   unsigned* ctr = reinterpret_cast<unsigned*>(ws);

@@ -254,6 +254,23 @@ class RecursiveSolver:
     # rows staged per device call: bounds the pinned and device staging buffers
     # (a continuation call is equivalent to one long call)
     _CHUNK_ROWS = 8192
+    # bytes per pipelined slice of a large call (0 disables the pipeline)
+    _SLICE_BYTES = 4 << 20
+
+    def _pipeline_rows(self, n):
+        """Rows per staging slice for a call of n rows, or 0 when one copy is
+        cheaper (a few slices at least, each a multiple of 32 rows)."""
+        if not self._SLICE_BYTES:
+            return 0
+        row_bytes = self._m * self._bs.dtype.itemsize
+        sub = max(32, (self._SLICE_BYTES // row_bytes) // 32 * 32)
+        return sub if n >= 2 * sub else 0
+
+    def _copy_stream(self):
+        cs = getattr(self, "_cs", None)
+        if cs is None:
+            cs = self._cs = self._torch.cuda.Stream(self._bs.device)
+        return cs
 
     def _run(self, A, y, want_report):
         n = A.shape[0]
@@ -270,16 +287,55 @@ class RecursiveSolver:
         m = self._m
         buf = self._buffers(n)
         esz = buf["esz"]
-        buf["rows_h_np"][:n] = A
-        buf["y_h_np"][:n] = y
         stream = torch.cuda.current_stream(bs.device)
         h = ctypes.c_void_p(stream.cuda_stream)
         cp = lib.rgb_memcpy_async
-        _lib.check(cp(buf["rows_d_p"], buf["rows_h_p"], n * m * esz, h), "rgb_memcpy_async")
-        _lib.check(cp(buf["y_d_p"], buf["y_h_p"], n * esz, h), "rgb_memcpy_async")
         ingest = lib.rgb_ingest_f32in if self._f32in else lib.rgb_ingest
         done = 0
         res = {}
+        sub = self._pipeline_rows(n)
+        if sub and not want_report and not self._trackers:
+            # a large plain ingest: stage it in slices -- the host copy of
+            # slice i+1 into pinned memory and its host-to-device copy (on a
+            # side stream) overlap the ingest of slice i; a stream that stops
+            # early (rank cap) skips the later slices and is resumed below
+            # from the rows already on the device
+            cs = self._copy_stream()
+            hc = ctypes.c_void_p(cs.cuda_stream)
+            cfg, st = self._structs()
+            for s0 in range(0, n, sub):
+                s1 = min(n, s0 + sub)
+                buf["rows_h_np"][s0:s1] = A[s0:s1]
+                buf["y_h_np"][s0:s1] = y[s0:s1]
+                _lib.check(cp(buf["rows_d_p"] + s0 * m * esz, buf["rows_h_p"] + s0 * m * esz,
+                              (s1 - s0) * m * esz, hc), "rgb_memcpy_async")
+                _lib.check(cp(buf["y_d_p"] + s0 * esz, buf["y_h_p"] + s0 * esz, (s1 - s0) * esz, hc),
+                           "rgb_memcpy_async")
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                stream.wait_event(ev)
+                _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["rows_d_p"] + s0 * m * esz, 0,
+                                  buf["y_d_p"] + s0 * esz, 0, s1 - s0, None, h), "rgb_ingest")
+            _lib.check(cp(buf["nobs_h_p"], bs.nobs_t.data_ptr(), 8, h), "rgb_memcpy_async")
+            _lib.check(cp(buf["cnt_h_p"], bs.rank_t.data_ptr(), 4, h), "rgb_memcpy_async")
+            _lib.check(cp(buf["cnt_h_p"] + 4, bs.status_t.data_ptr(), 4, h), "rgb_memcpy_async")
+            stream.synchronize()
+            nobs = int(buf["nobs_h_np"][0])
+            done = nobs - self._host["nobs"]
+            self._host["nobs"] = nobs
+            self._host["rank"] = int(buf["cnt_h_np"][0])
+            status = int(buf["cnt_h_np"][1])
+            if status & _lib.ST_RANK_CAP:
+                bs.grow(2 * bs.r_cap)
+                bs.status_t.zero_()
+            elif status:
+                bs.status_t.zero_()
+                raise ValueError(f"device status {status}: non-finite input or invalid rescaling factor")
+        else:
+            buf["rows_h_np"][:n] = A
+            buf["y_h_np"][:n] = y
+            _lib.check(cp(buf["rows_d_p"], buf["rows_h_p"], n * m * esz, h), "rgb_memcpy_async")
+            _lib.check(cp(buf["y_d_p"], buf["y_h_p"], n * esz, h), "rgb_memcpy_async")
         while done < n:
             T = n - done
             log_coords = bool(self._trackers)

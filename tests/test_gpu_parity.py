@@ -770,6 +770,27 @@ def test_dropin_solver_large_width_grows_capacity_on_the_grid_kernel():
     assert relerr(np.asarray(s.solution), oracle.solution(o)[0, :, 0]) <= 1e-9
 
 
+def test_dropin_large_call_pipeline_matches_single_copy():
+    """A large RecursiveSolver.ingest is staged in 4 MB slices whose copies
+    overlap the ingest of the previous slice; a rank-cap stop inside a slice
+    (capacity 32 -> 64 -> 128 here) resumes from the rows already on the device.
+    Same rank, x and nobs as the unsliced path and the oracle."""
+    from paper_2106_11594_b200 import RecursiveSolver
+
+    rows, tg = _lowrank_streams(1, 2000, 1024, 100, 1, seed=21)
+    o = oracle.ingest(rows, tg, r_cap=128, nthreads=1)
+    out = []
+    for slice_bytes in (4 << 20, 0):
+        s = RecursiveSolver(1024)
+        s._SLICE_BYTES = slice_bytes
+        assert bool(s._pipeline_rows(2000)) == bool(slice_bytes)
+        s.ingest(rows[0], tg[0, :, 0])
+        assert s.rank == int(o["rank"][0]) == 100 and s.num_observations == 2000
+        out.append(np.asarray(s.solution).copy())
+    assert relerr(out[0], oracle.solution(o)[0, :, 0]) <= 1e-9
+    assert relerr(out[0], out[1]) <= 1e-9
+
+
 @pytest.mark.parametrize("k", [1, 3, 7])
 def test_one_warp_kernel_fewer_right_hand_sides(k):
     """Config-5-shaped streams with k < 8 right-hand sides stay on the one-warp
