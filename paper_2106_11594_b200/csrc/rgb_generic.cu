@@ -46,7 +46,7 @@ __device__ __forceinline__ void block_reduce(int nv, REAL* red, REAL* out, F par
 template <typename REAL, typename TI>
 __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rows_stride,
-    const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs) {
+    const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs, int cached) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
   REAL* a_s = reinterpret_cast<REAL*>(smem_raw);        // m
@@ -58,19 +58,41 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
   REAL* sums = y_s + GEN_MAX_K;                          // k + 2: rej_sq, row_sq, a.x_c
   REAL* red = sums + GEN_MAX_K + 2;                      // GEN_NW x (GEN_MAX_K + 2)
   REAL* scal = red + GEN_NW * (GEN_MAX_K + 2);           // denom etc.
+  REAL* cache = scal + 8;  // cached: the stream's C, C~, P^-1, x (generic_cache_elems)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
   for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
-    REAL* C = reinterpret_cast<REAL*>(st.basis) + b * (int64_t)rc * m;
-    REAL* D = (var == RGB_ORTHONORMAL) ? C : reinterpret_cast<REAL*>(st.dual) + b * (int64_t)rc * m;
-    REAL* P = reinterpret_cast<REAL*>(st.gram_inv) + b * (int64_t)rc * rc;
-    REAL* X = reinterpret_cast<REAL*>(st.x) + b * (int64_t)k * m;
+    REAL* Cg = reinterpret_cast<REAL*>(st.basis) + b * (int64_t)rc * m;
+    REAL* Dg = (var == RGB_ORTHONORMAL) ? Cg : reinterpret_cast<REAL*>(st.dual) + b * (int64_t)rc * m;
+    REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv) + b * (int64_t)rc * rc;
+    REAL* Xg = reinterpret_cast<REAL*>(st.x) + b * (int64_t)k * m;
     const TI* R = rows + b * rows_stride;
     const TI* Y = targets + b * tg_stride;
     int r = st.rank[b];
     int status = st.status[b];
     int64_t nobs = st.nobs[b];
     if (status) continue;
+    const int r0 = r;
+    REAL *C = Cg, *D = Dg, *P = Pg, *X = Xg;
+    if (cached) {
+      // a state that fits in shared memory is read once, with every load in
+      // flight, instead of one dependent L2 round trip per step of every row
+      // (a one-row update() is a chain of such steps)
+      C = cache;
+      D = (var == RGB_ORTHONORMAL) ? C : C + (size_t)rc * m;
+      P = C + (size_t)(var == RGB_ORTHONORMAL ? 1 : 2) * rc * m;
+      X = P + (size_t)rc * rc;
+#pragma unroll 4
+      for (int e = tid; e < r0 * m; e += GEN_NT) C[e] = Cg[e];
+      if (var != RGB_ORTHONORMAL) {
+#pragma unroll 4
+        for (int e = tid; e < r0 * m; e += GEN_NT) D[e] = Dg[e];
+      }
+#pragma unroll 4
+      for (int e = tid; e < r0 * r0; e += GEN_NT) P[(e / r0) * rc + e % r0] = Pg[(e / r0) * rc + e % r0];
+#pragma unroll 4
+      for (int e = tid; e < k * m; e += GEN_NT) X[e] = Xg[e];
+    }
     for (int64_t t = 0; t < T; ++t) {
       const TI* a = R + t * m;
       for (int j = tid; j < m; j += GEN_NT) a_s[j] = (REAL)a[j];
@@ -206,6 +228,15 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
       __syncthreads();
     }
     __syncthreads();
+    if (cached) {  // write back what the rows changed (rows >= r0 are new; C~ and P^-1 change in place)
+      for (int e = tid; e < r * m; e += GEN_NT) {
+        if (e >= r0 * m) Cg[e] = C[e];
+        if (var != RGB_ORTHONORMAL) Dg[e] = D[e];
+      }
+      for (int e = tid; e < r * r; e += GEN_NT) Pg[(e / r) * rc + e % r] = P[(e / r) * rc + e % r];
+      for (int e = tid; e < k * m; e += GEN_NT) Xg[e] = X[e];
+      __syncthreads();
+    }
     if (tid == 0) {
       st.rank[b] = r;
       st.nobs[b] = nobs;
@@ -221,29 +252,42 @@ size_t generic_smem_bytes(const rgb_config& cfg) {
   return n * s;
 }
 
+// elements of the shared-memory copy of one stream's state
+static size_t generic_cache_elems(const rgb_config& cfg) {
+  const size_t m = cfg.m, rc = cfg.r_cap, k = cfg.k;
+  return (cfg.variant == RGB_ORTHONORMAL ? 1 : 2) * rc * m + rc * rc + k * m;
+}
+
+// the state is cached in shared memory when it fits in 96 KB (two CTAs per SM
+// stay resident for multi-stream calls)
+static constexpr size_t GEN_CACHE_MAX = 96 * 1024;
+
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms, bool f32in) {
   if (cfg.k > GEN_MAX_K) return RGB_E_UNSUPPORTED;
   size_t smem = generic_smem_bytes(cfg);
   if (smem > 200 * 1024) return RGB_E_UNSUPPORTED;
+  const size_t esz = cfg.dtype == RGB_F32 ? 4 : 8;
+  const int cached = smem + esz * generic_cache_elems(cfg) <= GEN_CACHE_MAX ? 1 : 0;
+  if (cached) smem += esz * generic_cache_elems(cfg);
   int64_t grid = cfg.num_streams < (int64_t)num_sms * 8 ? cfg.num_streams : (int64_t)num_sms * 8;
   if (grid < 1) return RGB_OK;
   if (cfg.dtype == RGB_F64 && f32in) {
     auto kern = generic_ingest_kernel<double, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                   (const float*)targets, tg_stride, T, logs);
+                                                   (const float*)targets, tg_stride, T, logs, cached);
   } else if (cfg.dtype == RGB_F64) {
     auto kern = generic_ingest_kernel<double, double>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                   (const double*)targets, tg_stride, T, logs);
+                                                   (const double*)targets, tg_stride, T, logs, cached);
   } else {
     auto kern = generic_ingest_kernel<float, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                  (const float*)targets, tg_stride, T, logs);
+                                                  (const float*)targets, tg_stride, T, logs, cached);
   }
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }

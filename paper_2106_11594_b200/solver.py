@@ -134,6 +134,7 @@ class RecursiveSolver:
         self._torch = torch
         self._f32in = False
         self._host = {"rank": 0, "nobs": 0}
+        self._graphs = {}  # one-row call graphs (None: capture unsupported)
 
     # -- read-only access ---------------------------------------------------
     @property
@@ -177,11 +178,34 @@ class RecursiveSolver:
     def project(self, row):
         """Coordinates of ``row`` in the stored basis plus its rejection."""
         row = self._kind.vector(row, self._m)
-        t = self._torch.as_tensor(row, device=self._bs.device).view(1, self._m)
-        coords, rej, rsq, _ = self._bs.project(t)
+        torch = self._torch
+        bs = self._bs
+        m, rc = self._m, bs.r_cap
+        buf = self._buffers(1)
+        esz = buf["esz"]
+        pb = getattr(self, "_pbuf", None)
+        if pb is None or pb[0] != rc:
+            # device block: coords [r_cap] | rejection [m] | rej_sq | dependent flag
+            nbytes = esz * (rc + m + 1) + 8
+            pd = torch.empty((nbytes,), dtype=torch.uint8, device=bs.device)
+            ph = torch.empty((nbytes,), dtype=torch.uint8, pin_memory=True)
+            npdt = np.float32 if bs.dtype == torch.float32 else np.float64
+            pb = self._pbuf = (rc, pd, ph, ph.numpy()[:esz * (rc + m + 1)].view(npdt))
+        _, pd, ph, pv = pb
+        buf["in_np"][:m] = row
+        stream = torch.cuda.current_stream(bs.device)
+        h = ctypes.c_void_p(stream.cuda_stream)
+        cp = bs.lib.rgb_memcpy_async
+        _lib.check(cp(buf["in_d_p"], buf["in_h_p"], m * esz, h), "rgb_memcpy_async")
+        cfg, st = self._structs()
+        base = pd.data_ptr()
+        _lib.check(bs.lib.rgb_project(ctypes.byref(cfg), ctypes.byref(st), buf["in_d_p"], base,
+                                      base + esz * rc, base + esz * (rc + m), base + esz * (rc + m + 1), h),
+                   "rgb_project")
+        _lib.check(cp(ph.data_ptr(), base, esz * (rc + m + 1), h), "rgb_memcpy_async")
+        stream.synchronize()
         r = self.rank
-        return ProjectionResult(coords[0, :r].cpu().numpy(), rej[0].cpu().numpy(),
-                                float(rsq[0].item()))
+        return ProjectionResult(pv[:r].copy(), pv[rc:rc + m].copy(), float(pv[rc + m]))
 
     def is_dependent(self, proj, row):
         """Rank test of solver.py:221-229 (a scalar decision, done on the host)."""
@@ -213,39 +237,58 @@ class RecursiveSolver:
     def _buffers(self, n):
         """Pinned host staging and device buffers for calls of up to n rows,
         reused across calls.  A per-row update() is latency bound, so a call is
-        one host-to-device copy per input, one ingest, asynchronous copies of
-        the counters and the report into pinned memory and one synchronisation,
-        all through raw pointers (librgb's rgb_memcpy_async)."""
+        one host-to-device copy (rows and targets packed in one block), one
+        ingest, one device-to-host copy of a packed report block and one
+        synchronisation, all through raw pointers (librgb's rgb_memcpy_async).
+
+        Report block (bytes): nobs int64 | rank int32 | status int32 | gain
+        [m] | branch [cap, padded to 8] | resid [cap].  The solver's counters
+        live at its head (rebound on every reallocation), so the one copy
+        brings back the counters with the report."""
         torch = self._torch
         buf = getattr(self, "_buf", None)
         if buf is not None and buf["cap"] >= n:
             return buf
         cap = 1 << max(0, (n - 1).bit_length())
-        dev, dt, m = self._bs.device, self._bs.dtype, self._m
+        bs = self._bs
+        dev, dt, m = bs.device, bs.dtype, self._m
+        esz = torch.empty((), dtype=dt).element_size()
+        off_gain = 16
+        off_branch = off_gain + esz * m
+        off_resid = off_branch + (cap + 7) // 8 * 8
+        nbytes = off_resid + esz * cap
         t = {
-            "rows_h": torch.empty((cap, m), dtype=dt, pin_memory=True),
-            "y_h": torch.empty((cap,), dtype=dt, pin_memory=True),
-            "rows_d": torch.empty((cap, m), dtype=dt, device=dev),
-            "y_d": torch.empty((cap,), dtype=dt, device=dev),
-            "branch_d": torch.empty((1, cap), dtype=torch.uint8, device=dev),
-            "resid_d": torch.empty((1, cap, 1), dtype=dt, device=dev),
-            "gain_d": torch.empty((1, m), dtype=dt, device=dev),
-            "branch_h": torch.empty((cap,), dtype=torch.uint8, pin_memory=True),
-            "resid_h": torch.empty((cap,), dtype=dt, pin_memory=True),
-            "gain_h": torch.empty((m,), dtype=dt, pin_memory=True),
-            "nobs_h": torch.empty((1,), dtype=torch.int64, pin_memory=True),
-            "cnt_h": torch.empty((2,), dtype=torch.int32, pin_memory=True),
+            "in_h": torch.empty((cap * (m + 1),), dtype=dt, pin_memory=True),
+            "in_d": torch.empty((cap * (m + 1),), dtype=dt, device=dev),
+            "io_h": torch.zeros((nbytes,), dtype=torch.uint8, pin_memory=True),
+            "io_d": torch.zeros((nbytes,), dtype=torch.uint8, device=dev),
         }
-        buf = {"cap": cap, "t": t, "esz": t["y_h"].element_size()}
-        buf.update({k + "_np": v.numpy() for k, v in t.items() if not k.endswith("_d")})
+        io = t["io_d"]
+        if buf is not None:
+            io[:16].copy_(buf["t"]["io_d"][:16])
+        else:
+            io[0:8].view(torch.int64).copy_(bs.nobs_t)
+            io[8:12].view(torch.int32).copy_(bs.rank_t)
+            io[12:16].view(torch.int32).copy_(bs.status_t)
+        bs.nobs_t = io[0:8].view(torch.int64)
+        bs.rank_t = io[8:12].view(torch.int32)
+        bs.status_t = io[12:16].view(torch.int32)
+        ioh = t["io_h"].numpy()
+        npdt = np.dtype(np.float32 if dt == torch.float32 else np.float64)
+        buf = {"cap": cap, "t": t, "esz": esz, "off_gain": off_gain, "off_branch": off_branch,
+               "off_resid": off_resid, "in_np": t["in_h"].numpy(),
+               "nobs_np": ioh[0:8].view(np.int64), "cnt_np": ioh[8:16].view(np.int32),
+               "gain_np": ioh[off_gain:off_branch].view(npdt), "branch_np": ioh[off_branch:off_branch + cap],
+               "resid_np": ioh[off_resid:].view(npdt)}
         buf.update({k + "_p": v.data_ptr() for k, v in t.items()})
         self._buf = buf
         return buf
 
     def _structs(self):
-        """rgb_config / rgb_state of the single stream, rebuilt when the capacity grows."""
+        """rgb_config / rgb_state of the single stream, rebuilt when the capacity
+        grows or the counters move."""
         bs = self._bs
-        key = (bs.r_cap, bs.basis_t.data_ptr())
+        key = (bs.r_cap, bs.basis_t.data_ptr(), bs.nobs_t.data_ptr())
         if getattr(self, "_st_key", None) != key:
             self._st = (bs.config(), bs.state())
             self._st_key = key
@@ -287,6 +330,25 @@ class RecursiveSolver:
         m = self._m
         buf = self._buffers(n)
         esz = buf["esz"]
+        in_h, in_d = buf["in_h_p"], buf["in_d_p"]
+        io_h, io_d = buf["io_h_p"], buf["io_d_p"]
+        y_off = n * m  # the targets follow the rows in the staging block
+        if n == 1 and not self._trackers and self._graphs is not None:
+            # a per-row call: one replay of a captured copy-ingest-copy graph
+            g = self._row_graph(buf, want_report)
+            if g is not None:
+                buf["in_np"][:m] = A[0]
+                buf["in_np"][m] = y[0]
+                g.replay()
+                torch.cuda.current_stream(bs.device).synchronize()
+                consumed, status = self._take_counters(buf)
+                if consumed:
+                    self._on_status(status)
+                    if want_report:
+                        return {"branch": buf["branch_np"][:1].copy(), "resid": buf["resid_np"][:1].copy(),
+                                "gain": buf["gain_np"].copy()}
+                    return {}
+                self._on_status(status)  # rank cap: grown; the row runs again below
         stream = torch.cuda.current_stream(bs.device)
         h = ctypes.c_void_p(stream.cuda_stream)
         cp = lib.rgb_memcpy_async
@@ -305,37 +367,25 @@ class RecursiveSolver:
             cfg, st = self._structs()
             for s0 in range(0, n, sub):
                 s1 = min(n, s0 + sub)
-                buf["rows_h_np"][s0:s1] = A[s0:s1]
-                buf["y_h_np"][s0:s1] = y[s0:s1]
-                _lib.check(cp(buf["rows_d_p"] + s0 * m * esz, buf["rows_h_p"] + s0 * m * esz,
-                              (s1 - s0) * m * esz, hc), "rgb_memcpy_async")
-                _lib.check(cp(buf["y_d_p"] + s0 * esz, buf["y_h_p"] + s0 * esz, (s1 - s0) * esz, hc),
+                buf["in_np"][s0 * m:s1 * m] = A[s0:s1].reshape(-1)
+                buf["in_np"][y_off + s0:y_off + s1] = y[s0:s1]
+                _lib.check(cp(in_d + s0 * m * esz, in_h + s0 * m * esz, (s1 - s0) * m * esz, hc),
+                           "rgb_memcpy_async")
+                _lib.check(cp(in_d + (y_off + s0) * esz, in_h + (y_off + s0) * esz, (s1 - s0) * esz, hc),
                            "rgb_memcpy_async")
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 stream.wait_event(ev)
-                _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["rows_d_p"] + s0 * m * esz, 0,
-                                  buf["y_d_p"] + s0 * esz, 0, s1 - s0, None, h), "rgb_ingest")
-            _lib.check(cp(buf["nobs_h_p"], bs.nobs_t.data_ptr(), 8, h), "rgb_memcpy_async")
-            _lib.check(cp(buf["cnt_h_p"], bs.rank_t.data_ptr(), 4, h), "rgb_memcpy_async")
-            _lib.check(cp(buf["cnt_h_p"] + 4, bs.status_t.data_ptr(), 4, h), "rgb_memcpy_async")
+                _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), in_d + s0 * m * esz, 0,
+                                  in_d + (y_off + s0) * esz, 0, s1 - s0, None, h), "rgb_ingest")
+            _lib.check(cp(io_h, io_d, 16, h), "rgb_memcpy_async")
             stream.synchronize()
-            nobs = int(buf["nobs_h_np"][0])
-            done = nobs - self._host["nobs"]
-            self._host["nobs"] = nobs
-            self._host["rank"] = int(buf["cnt_h_np"][0])
-            status = int(buf["cnt_h_np"][1])
-            if status & _lib.ST_RANK_CAP:
-                bs.grow(2 * bs.r_cap)
-                bs.status_t.zero_()
-            elif status:
-                bs.status_t.zero_()
-                raise ValueError(f"device status {status}: non-finite input or invalid rescaling factor")
+            done, status = self._take_counters(buf)
+            self._on_status(status)
         else:
-            buf["rows_h_np"][:n] = A
-            buf["y_h_np"][:n] = y
-            _lib.check(cp(buf["rows_d_p"], buf["rows_h_p"], n * m * esz, h), "rgb_memcpy_async")
-            _lib.check(cp(buf["y_d_p"], buf["y_h_p"], n * esz, h), "rgb_memcpy_async")
+            buf["in_np"][:y_off] = A.reshape(-1)
+            buf["in_np"][y_off:y_off + n] = y
+            _lib.check(cp(in_d, in_h, (y_off + n) * esz, h), "rgb_memcpy_async")
         while done < n:
             T = n - done
             log_coords = bool(self._trackers)
@@ -343,41 +393,89 @@ class RecursiveSolver:
             # routes the call to the generic kernel (the tensor-core kernels
             # do not log them); every log entry of a consumed row is written
             coords = torch.zeros((1, T, bs.r_cap), dtype=bs.dtype, device=bs.device) if log_coords else None
-            logs = _lib.Logs(buf["branch_d_p"] if want_report else None,
+            logs = _lib.Logs(io_d + buf["off_branch"] if want_report else None,
                              coords.data_ptr() if log_coords else None,
-                             buf["resid_d_p"] if want_report else None,
-                             buf["gain_d_p"] if want_report else None)
+                             io_d + buf["off_resid"] if want_report else None,
+                             io_d + buf["off_gain"] if want_report else None)
             cfg, st = self._structs()
-            _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["rows_d_p"] + done * m * esz, T * m,
-                              buf["y_d_p"] + done * esz, T, T, ctypes.byref(logs), h), "rgb_ingest")
-            # counters and report: asynchronous copies into pinned memory, one sync
-            _lib.check(cp(buf["nobs_h_p"], bs.nobs_t.data_ptr(), 8, h), "rgb_memcpy_async")
-            _lib.check(cp(buf["cnt_h_p"], bs.rank_t.data_ptr(), 4, h), "rgb_memcpy_async")
-            _lib.check(cp(buf["cnt_h_p"] + 4, bs.status_t.data_ptr(), 4, h), "rgb_memcpy_async")
-            if want_report:
-                _lib.check(cp(buf["branch_h_p"], buf["branch_d_p"], T, h), "rgb_memcpy_async")
-                _lib.check(cp(buf["resid_h_p"], buf["resid_d_p"], T * esz, h), "rgb_memcpy_async")
-                _lib.check(cp(buf["gain_h_p"], buf["gain_d_p"], m * esz, h), "rgb_memcpy_async")
+            _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), in_d + done * m * esz, T * m,
+                              in_d + (y_off + done) * esz, T, T, ctypes.byref(logs), h), "rgb_ingest")
+            # counters (and the report): one asynchronous copy into pinned memory, one sync
+            nb = buf["off_resid"] + T * esz if want_report else 16
+            _lib.check(cp(io_h, io_d, nb, h), "rgb_memcpy_async")
             stream.synchronize()
-            nobs = int(buf["nobs_h_np"][0])
-            rank, status = int(buf["cnt_h_np"][0]), int(buf["cnt_h_np"][1])
-            consumed = nobs - self._host["nobs"]
-            self._host["nobs"] = nobs
-            self._host["rank"] = rank
+            consumed, status = self._take_counters(buf)
             if log_coords and consumed:
                 self._coords_chunks.append(coords[0, :consumed].cpu().numpy())
             if want_report:
-                res = {"branch": buf["branch_h_np"][:consumed].copy(),
-                       "resid": buf["resid_h_np"][:consumed].copy(),
-                       "gain": buf["gain_h_np"].copy()}
+                res = {"branch": buf["branch_np"][:consumed].copy(),
+                       "resid": buf["resid_np"][:consumed].copy(),
+                       "gain": buf["gain_np"].copy()}
             done += consumed
-            if status & _lib.ST_RANK_CAP:
-                bs.grow(2 * bs.r_cap)
-                bs.status_t.zero_()
-            elif status:
-                bs.status_t.zero_()
-                raise ValueError(f"device status {status}: non-finite input or invalid rescaling factor")
+            self._on_status(status)
         return res
+
+    def _row_graph(self, buf, want_report):
+        """CUDA graph of a one-row call -- host-to-device copy of the staged row
+        and target, rgb_ingest (T = 1, with the report logs for update()), and
+        the device-to-host copy of the counters and report -- captured once per
+        buffer and capacity layout, so update() costs one graph launch and one
+        synchronisation.  None (and graphs off) if capture fails."""
+        torch = self._torch
+        bs = self._bs
+        cfg, st = self._structs()
+        key = (want_report, self._st_key, buf["in_d_p"], buf["io_d_p"])
+        g = self._graphs.get(key)
+        if g is not None:
+            return g
+        self._graphs.clear()  # a layout change invalidates the older graphs
+        m, esz = self._m, buf["esz"]
+        io_d = buf["io_d_p"]
+        logs = _lib.Logs(io_d + buf["off_branch"] if want_report else None, None,
+                         io_d + buf["off_resid"] if want_report else None,
+                         io_d + buf["off_gain"] if want_report else None)
+        ingest = bs.lib.rgb_ingest_f32in if self._f32in else bs.lib.rgb_ingest
+        cp = bs.lib.rgb_memcpy_async
+        nb = buf["off_resid"] + esz if want_report else 16
+        gs = torch.cuda.Stream(bs.device)
+        g = torch.cuda.CUDAGraph()
+        rcs = []
+        try:
+            with torch.cuda.graph(g, stream=gs, capture_error_mode="thread_local"):
+                h = ctypes.c_void_p(gs.cuda_stream)
+                rcs.append(cp(buf["in_d_p"], buf["in_h_p"], (m + 1) * esz, h))
+                rcs.append(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["in_d_p"], m,
+                                  buf["in_d_p"] + m * esz, 1, 1, ctypes.byref(logs), h))
+                rcs.append(cp(buf["io_h_p"], io_d, nb, h))
+        except RuntimeError:
+            rcs.append(-1)
+        if any(rcs):
+            self._graphs = None
+            return None
+        g._rgb_keep = (logs, cfg, st)  # the captured launch read these structs
+        self._graphs[key] = g
+        return g
+
+    def _take_counters(self, buf):
+        """Counters of the last report copy: records nobs and rank; returns
+        (rows consumed since the previous read, status bits)."""
+        nobs = int(buf["nobs_np"][0])
+        rank, status = int(buf["cnt_np"][0]), int(buf["cnt_np"][1])
+        consumed = nobs - self._host["nobs"]
+        self._host["nobs"] = nobs
+        self._host["rank"] = rank
+        return consumed, status
+
+    def _on_status(self, status):
+        """A rank-cap stop doubles the capacity (the caller resumes); any other
+        stop (invalid rescaling factor) raises."""
+        bs = self._bs
+        if status & _lib.ST_RANK_CAP:
+            bs.grow(2 * bs.r_cap)
+            bs.status_t.zero_()
+        elif status:
+            bs.status_t.zero_()
+            raise ValueError(f"device status {status}: non-finite input or invalid rescaling factor")
 
 
 def solve_batch(matrix, targets, *, variant="general", eps=None, scalar=FLOAT64, alpha=1):
