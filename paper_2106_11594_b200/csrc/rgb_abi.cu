@@ -3,7 +3,9 @@
 // Validation mirrors the reference's constructor and input checks
 // (solver.py:142-158, scalars.py:108-138) as return codes.  Dispatch, first
 // match wins: the one-warp tensor-core kernel (m 64, r_cap 16, k <= 8), the
-// warp-group kernel (m 128 / r_cap 32, m 256 / r_cap 16), the cluster kernel
+// panel kernel (m 128, r_cap 16 / 32, general variant; RGB_NO_PANEL=1 in the
+// environment turns it off, for A/B runs and tests), the warp-group kernel
+// (m 128 / r_cap 32, m 256 / r_cap 16, every variant), the cluster kernel
 // (r_cap 64, m <= 1 080) and the grid kernel (a few large streams, m <= 2 368,
 // r_cap <= 512) -- the last two for calls of 8+ rows -- and the shape-generic
 // kernel for everything else, for fp32 state and for per-row residual logs.
@@ -11,6 +13,7 @@
 // stream-ordered, from a library-owned device memory pool that is kept
 // between calls).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "rgb_common.cuh"
@@ -21,6 +24,9 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
                    cudaStream_t stream, int num_sms, bool f32in);
 bool blocked_supports(const rgb_config& cfg);
 bool blocked_wg_supports(const rgb_config& cfg);
+bool panel_supports(const rgb_config& cfg);
+int launch_panel(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
+                 int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms, bool f32in);
 bool grid_supports(const rgb_config& cfg);
 bool cluster_supports(const rgb_config& cfg);
 int launch_cluster(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
@@ -76,6 +82,11 @@ static int check_state(const rgb_config* cfg, const rgb_state* st) {
     return fail(RGB_E_INVALID, "null state buffer");
   if (cfg->variant != RGB_ORTHONORMAL && !st->dual) return fail(RGB_E_INVALID, "null dual buffer");
   return RGB_OK;
+}
+
+static bool env_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && strcmp(v, "0") != 0;
 }
 
 static int sm_count() {
@@ -141,6 +152,8 @@ static int ingest_impl(const rgb_config* cfg, rgb_state* st, const void* rows, i
   rc = RGB_E_UNSUPPORTED;
   if (rgb::blocked_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
+  else if (rgb::panel_supports(*cfg) && !lg.resid && !lg.gain && !env_flag("RGB_NO_PANEL"))
+    rc = rgb::launch_panel(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::blocked_wg_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked_wg(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   // the multi-SM kernels pay microseconds of setup and barriers per call: a

@@ -259,6 +259,43 @@ def test_c3_full_length_streams_against_oracle():
     assert amb <= 1
 
 
+@pytest.mark.parametrize("kernel", ["panel", "warp-group"])
+def test_c3_kernels_against_oracle_and_each_other(kernel, monkeypatch):
+    """Config-3 streams (m 128, r_cap 32, general variant) through the panel
+    kernel (the default dispatch) and, with RGB_NO_PANEL set, through the
+    warp-group kernel: oracle ranks / branches on unambiguous streams, x within
+    the fp64 bar, partial-tile continuation calls equal to one call, and the two
+    kernels agree with each other."""
+    from paper_2106_11594_b200 import workloads
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    if kernel == "warp-group":
+        monkeypatch.setenv("RGB_NO_PANEL", "1")
+    rows, tg = workloads.host_batch("c3", list(range(40, 64)), n=300)
+    res = run_batched(rows, tg, r_cap=32)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=32)
+    assert amb <= 1 and worst <= 1e-10
+    B, n, m = rows.shape
+    bs = BatchedSolver(B, m, k=1, r_cap=32)
+    lo = 0
+    for hi in (5, 8, 29, 100, 217, 300):
+        bs.ingest(dev(np.ascontiguousarray(rows[:, lo:hi])), dev(np.ascontiguousarray(tg[:, lo:hi])))
+        lo = hi
+    torch.cuda.synchronize()
+    assert np.array_equal(bs.rank.cpu().numpy(), res["rank"])
+    X = bs.solution.cpu().numpy()
+    assert max(relerr(X[i], res["x"][i]) for i in range(B)) <= 1e-10
+    if kernel == "panel":
+        monkeypatch.setenv("RGB_NO_PANEL", "1")
+    else:
+        monkeypatch.delenv("RGB_NO_PANEL")
+    other = run_batched(rows, tg, r_cap=32)
+    same = res["rank"] == other["rank"]
+    assert same.mean() >= 0.95
+    for i in np.nonzero(same)[0]:
+        assert relerr(other["x"][i], res["x"][i]) <= 1e-10
+
+
 def test_c5_short_streams_ill_conditioned_start():
     """256-row prefixes: the first dependent tiles see the least-conditioned
     8x8 systems (large coordinates on a fresh 16-row basis)."""
