@@ -45,6 +45,8 @@
 //   -C     Cf[kt][jt][lane]  = -C[sigma(kt,q)][8jt+p]    shared memory (B operand of R)
 //   P^-1   Pr[mt][nt][e]     = P[8mt+p][8nt+2q+e]        home registers (symmetric)
 //   W^T    Wt[mt][e]         = W[8mt+2q+e][c=p]          home registers
+#include <type_traits>
+
 #include "rgb_mma.cuh"
 
 namespace rgb {
@@ -211,7 +213,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
     // warps, the rejection of the own columns 8J + p, its norm summed the same
     // way, and the growth applied by every warp to its own columns.
     if (fresh && !has_x0) {
-      constexpr int NRW = PW + 1, NGR = (NJ + NRW - 1) / NRW;
+      constexpr int NRW = PW + 1, NGR = NJ / NRW;
+      static_assert(NJ % NRW == 0, "row mode: whole column groups per warp");
       const int u = threadIdx.x >> 5;
       double esq = eps_sq<double>(cfg, r);
       double2 nx[NGR];
@@ -222,14 +225,16 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
           for (int jj = 0; jj < NGR; ++jj) {
             const int J = u + NRW * jj;
-            nx[jj] = (J < NJ) ? ld2(ar + 8 * J + 2 * q) : make_double2(0.0, 0.0);
+            nx[jj] = ld2(ar + 8 * J + 2 * q);
           }
           nyv = (p < k) ? (double)Yb[t * k + p] : 0.0;  // y[c = p]
         }
       };
       load_row(0);
-      while (tcur < T && r < R) {
-        const int nti = (r + 7) >> 3;
+      // the row step, specialised on the number of nonzero rank tiles (the
+      // unrolled loops then carry no predicated-off work)
+      auto row_step = [&](auto NTc) -> bool {
+        constexpr int nti = decltype(NTc)::value;
         double2 av[NGR];
 #pragma unroll
         for (int jj = 0; jj < NGR; ++jj) av[jj] = nx[jj];
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
         for (int jj = 0; jj < NGR; ++jj) {
           const int J = u + NRW * jj;
-          if (J < NJ) {
+          {
             a2 = fma(av[jj].x, av[jj].x, fma(av[jj].y, av[jj].y, a2));
 #pragma unroll
             for (int nt = 0; nt < IT; ++nt) {
@@ -274,7 +279,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
         for (int nt = 0; nt < IT; ++nt) {
           gfull[nt] = 0.0;
-          if (nt <= (r >> 3)) {
+          if (nt <= nti && nt <= (r >> 3)) {
 #pragma unroll
             for (int v = 0; v < NRW; ++v) gfull[nt] += S.gpart[v][8 * nt + p];
           }
@@ -296,13 +301,13 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
           double rp = 0.0;
 #pragma unroll
           for (int kt = 0; kt < IK; ++kt)
-            if ((kt >> 1) < nti && J < NJ) rp = fma(gk[kt], S.Cf[kt][J][lane], rp);  // Cf = -C
+            if ((kt >> 1) < nti) rp = fma(gk[kt], S.Cf[kt][J][lane], rp);  // Cf = -C
           rp += __shfl_xor_sync(FULL, rp, 1);
           rp += __shfl_xor_sync(FULL, rp, 2);
           const double v0 = __shfl_sync(FULL, av[jj].x, p >> 1);
           const double v1 = __shfl_sync(FULL, av[jj].y, p >> 1);
           aj[jj] = (p & 1) ? v1 : v0;
-          rej[jj] = aj[jj] + rp;  // zero for groups past NJ
+          rej[jj] = aj[jj] + rp;
           r2 = fma(rej[jj], rej[jj], r2);
         }
         r2 += __shfl_xor_sync(FULL, r2, 4);
@@ -314,14 +319,14 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
         for (int v = 0; v < NRW; ++v) rsq += S.r2part[v];
         const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
-        if (bad || is_dependent<double>(rsq, asq, esq)) break;  // panel mode takes this row
+        if (bad || is_dependent<double>(rsq, asq, esq)) return false;  // panel mode takes this row
         // growth (general variant): K = rej / |rej|^2, C~[:r] -= gamma K^T,
         // C~[r] = K, C[r] = a, W[r] = y (x0 = 0), P^-1 = diag(P^-1, 1)
         const double rinv = 1.0 / rsq;  // one rounding more than a division, as every kernel
         if (q == 0) {
 #pragma unroll
           for (int jj = 0; jj < NGR; ++jj)
-            if (u + NRW * jj < NJ) S.kv[8 * (u + NRW * jj) + p] = rej[jj] * rinv;
+            S.kv[8 * (u + NRW * jj) + p] = rej[jj] * rinv;
         }
         __syncwarp();
         {
@@ -329,22 +334,22 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
           for (int kk = 0; kk < 2 * NGR; ++kk) {
             const int J = u + NRW * (kk >> 1);
-            kvr[kk] = (J < NJ) ? S.kv[sigma(2 * J + (kk & 1), q)] : 0.0;
+            kvr[kk] = S.kv[sigma(2 * J + (kk & 1), q)];
           }
 #pragma unroll
           for (int nt = 0; nt < IT; ++nt) {
-            if (nt > (r >> 3)) break;
+            if (nt > nti || nt > (r >> 3)) break;
             const int i = 8 * nt + p;
             double dv[2 * NGR];
 #pragma unroll
             for (int kk = 0; kk < 2 * NGR; ++kk) {
               const int J = u + NRW * (kk >> 1);
-              dv[kk] = (J < NJ) ? S.Df[nt][2 * J + (kk & 1)][lane] : 0.0;
+              dv[kk] = S.Df[nt][2 * J + (kk & 1)][lane];
             }
 #pragma unroll
             for (int kk = 0; kk < 2 * NGR; ++kk) {
               const int J = u + NRW * (kk >> 1);
-              if (J < NJ) S.Df[nt][2 * J + (kk & 1)][lane] = (i == r) ? kvr[kk] : fma(-gfull[nt], kvr[kk], dv[kk]);
+              S.Df[nt][2 * J + (kk & 1)][lane] = (i == r) ? kvr[kk] : fma(-gfull[nt], kvr[kk], dv[kk]);
             }
           }
         }
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
           const int ktr = 2 * (r >> 3) + (r & 1);
 #pragma unroll
           for (int jj = 0; jj < NGR; ++jj)
-            if (u + NRW * jj < NJ) S.Cf[ktr][u + NRW * jj][lane] = -aj[jj];
+            S.Cf[ktr][u + NRW * jj][lane] = -aj[jj];
         }
         if (u == 0) {
           if (q == 0) S.Wsm[r][p] = yv;  // 0 for c >= k
@@ -363,6 +368,16 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
         r += 1;
         esq = eps_sq<double>(cfg, r);
         ++tcur;
+        return true;
+      };
+      while (tcur < T && r < R) {
+        const int nt_rt = (r + 7) >> 3;
+        bool go;
+        if (nt_rt <= 1) go = row_step(std::integral_constant<int, 1>{});
+        else if (nt_rt == 2) go = row_step(std::integral_constant<int, (2 < IT ? 2 : IT)>{});
+        else if (nt_rt == 3) go = row_step(std::integral_constant<int, (3 < IT ? 3 : IT)>{});
+        else go = row_step(std::integral_constant<int, IT>{});
+        if (!go) break;
       }
       __syncthreads();  // every warp's columns of C~ / C are in
       PPROBE(1);
