@@ -1008,10 +1008,17 @@ def test_random_shapes_against_oracle(seed):
 
 @pytest.mark.parametrize("m,r_cap", [(128, 16), (256, 32)])
 @pytest.mark.parametrize("variant", ["general", "orthonormal"])
-def test_warp_group_kernel_other_instantiations(m, r_cap, variant):
+@pytest.mark.parametrize("no_panel", [False, True])
+def test_warp_group_kernel_other_instantiations(m, r_cap, variant, no_panel, monkeypatch):
     """Warp-group kernel at m 128 / r_cap 16 (4 warps, two own a P block) and
-    m 256 / r_cap 32 (8 warps): many streams, ranks up to the capacity."""
+    m 256 / r_cap 32 (8 warps): many streams, ranks up to the capacity.  The
+    general variant at m 128 runs on the panel kernel unless RGB_NO_PANEL is set."""
     from paper_2106_11594_b200.batched import BatchedSolver
+
+    if no_panel:
+        if m != 128 or variant != "general":
+            pytest.skip("the panel kernel serves only the general variant at m = 128")
+        monkeypatch.setenv("RGB_NO_PANEL", "1")
 
     B, n = 24, 200
     rng = np.random.default_rng(m + r_cap)
