@@ -16,7 +16,9 @@ from paper_2106_11594_b200 import workloads  # noqa: E402
 from paper_2106_11594_b200.batched import BatchedSolver  # noqa: E402
 
 
-def sweep(cfg_name, B):
+def sweep(cfg_name, B, kernel="default"):
+    """kernel: "default" (the dispatcher's choice) or "warp-group" (RGB_NO_PANEL=1)."""
+    os.environ["RGB_NO_PANEL"] = "1" if kernel == "warp-group" else "0"
     c = workloads.CONFIGS[cfg_name]
     rows_d, tg_d = workloads.device_batch(cfg_name, 0, B, "cuda")
     n = rows_d.shape[1]
@@ -33,7 +35,8 @@ def sweep(cfg_name, B):
     rank = bs.rank.cpu().numpy()
     X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
     err = np.abs(X - XO).max(axis=(1, 2)) / np.maximum(1.0, np.abs(XO).max(axis=(1, 2)))
-    return {"config": cfg_name, "streams": B, "rows_per_stream": n,
+    return {"config": cfg_name, "kernel": {"c5": "one-warp", "c3": "panel"}[cfg_name] if kernel == "default" else kernel,
+            "streams": B, "rows_per_stream": n,
             "ambiguous_or_runaway": int(amb.sum()), "device_frozen": int((dev_status != 0).sum()),
             "checked": int(ok.sum()),
             "branch_mismatch": int((branch[ok] != o["branch"][ok]).any(axis=1).sum()),
@@ -42,7 +45,7 @@ def sweep(cfg_name, B):
             "tolerance": 1e-9}
 
 
-out = [sweep("c5", 16384), sweep("c3", 4096)]
+out = [sweep("c5", 16384), sweep("c3", 4096), sweep("c3", 4096, "warp-group")]
 print(json.dumps(out, indent=1))
 path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "parity_sweep.json")
 json.dump(out, open(path, "w"), indent=1)
