@@ -12,7 +12,9 @@
 //  * Three PROJECTION warps take a 24-row panel, one 8-row tile each, and run
 //    the whole projection of their tile -- G = A C~^T, R = A - G C, |a|^2,
 //    |R_t|^2 and the rank test (solver.py:286-296) -- over all m columns with
-//    no cross-warp reduction.  Inside a run of dependent rows C~ and C do not
+//    no cross-warp reduction.  A tile goes from global memory straight into
+//    the MMA fragment registers; the next panel's rows are pulled into L2
+//    (prefetch.global.L2) meanwhile.  Inside a run of dependent rows C~ and C do not
 //    change, so the three tiles are independent; the first independent (or
 //    non-finite) row of the panel ends it: the rows before it are dependent,
 //    the row grows the basis (solver.py:305-318, _grow :368-397; every warp
@@ -32,12 +34,15 @@
 //    shared memory.
 //
 // General variant, fp64 state, k <= 8 right-hand sides, float64 or float32
-// inputs; instantiated for m = 128 with r_cap 16 and 32.  Two CTAs (two
-// streams, eight warps) per SM.  Measured on config 3 (scripts/probe_panel.py,
-// -DRGB_PANEL_PROBE): 2.67 ms against 3.11 ms for the warp-group kernel; per
-// stream the row mode is ~1/3 of the time, and the home warp's chain (8x8
-// LDL^T ~1 900 cycles per tile behind the projection warps' DMMAs) bounds the
-// panel phase.
+// inputs; instantiated for m = 128 with r_cap 16 and 32.  Three CTAs (three
+// streams, twelve warps) per SM: 74 KB of shared memory and at most 168
+// registers per thread; W's rows share the hand-off slot's memory (the home
+// warp reads them before the first panel and writes W there after the last).
+// Config 3: 2.35 ms against 3.11 ms for the warp-group kernel (2.60 ms with two
+// CTAs per SM and a cp.async stage per warp).  Per stream (scripts/probe_panel.py,
+// -DRGB_PANEL_PROBE) the row mode is ~1/3 of the time, and the home warp's chain
+// (8x8 LDL^T ~1 900 cycles per tile behind the projection warps' DMMAs) bounds
+// the panel phase.
 //
 // Fragment layouts (lane = 4p + q; sigma(kt,q) = 8(kt>>1) + 2q + (kt&1)):
 //   tile   acc[jt][e]        = A[t=p][8jt+2q+e]         registers (A- and B-operand, K = sigma)
@@ -128,13 +133,12 @@ struct PanelSmem {
   static constexpr int IT = R / 8, IK = R / 4, NJ = M / 8, KS = M / 4;
   double Df[IT][KS][32];       // C~, B-fragment order
   double Cf[IK][NJ][32];       // -C, B-fragment order
-  TI At[PW][NJ][32][2];        // staged tile of each projection warp (next panel)
   // hand-off slot: one panel, projection warps -> home warp
   double sG[PW][IT][32][2];    // G of each tile (accumulator layout)
   double sDy[PW][32][2];       // y - a.x0, [c=p][t=2q+e]
   double sWnew[8];             // growth: W's new row (per RHS)
   int sTe[PW];                 // dependent rows [0, te) of each tile
-  int sGrow, sEnd, sR0;        // growth marker, end of stream, rank before the panel
+  int sGrow, sEnd;             // growth marker, end of stream
   // projection-warp exchange
   int stop[PW];                // first stop row of each tile (TT = none)
   int bad[PW];                 // ... and whether it is non-finite
@@ -142,11 +146,10 @@ struct PanelSmem {
   double a2part[PW + 1], r2part[PW + 1];
   double gam[R];               // growth: coords of the row
   double kv[M];                //         its gain K = rej / |rej|^2
-  double Wsm[R][8];            // W rows of the row-mode phase; W at the end
 };
 
 template <int R, int M, typename TI>
-__global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
+__global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
     const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
     double* __restrict__ clog) {
@@ -158,6 +161,10 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
   static_assert(R % 8 == 0 && R <= 32 && M % 8 == 0 && PW == 3, "shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SMT& S = *reinterpret_cast<SMT*>(smem_raw);
+  // W rows of the row-mode phase / W at the end share the hand-off slot (the
+  // home warp reads them before the first panel and writes them after the last)
+  static_assert(sizeof(S.sG) >= sizeof(double) * R * 8, "W over the slot");
+  double (&Wsm)[R][8] = *reinterpret_cast<double(*)[R][8]>(&S.sG[0][0][0][0]);
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;  // warps 0..PW-1 project, warp PW is the home warp
   const int p = lane >> 2, q = lane & 3;
@@ -195,7 +202,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
       const int l = i & 31, jt = (i >> 5) % NJ, kt = (i >> 5) / NJ;
       (&S.Cf[0][0][0])[i] = fresh ? 0.0 : -Cg[sigma(kt, l & 3) * M + 8 * jt + (l >> 2)];
     }
-    for (int i = threadIdx.x; i < R * 8; i += PANEL_THREADS) (&S.Wsm[0][0])[i] = 0.0;
+    for (int i = threadIdx.x; i < R * 8; i += PANEL_THREADS) (&Wsm[0][0])[i] = 0.0;
     bool nz = false;
     if (!fresh)
       for (int i = threadIdx.x; i < k * M; i += PANEL_THREADS) nz |= (Xg[i] != 0.0);
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
             S.Cf[ktr][u + NRW * jj][lane] = -aj[jj];
         }
         if (u == 0) {
-          if (q == 0) S.Wsm[r][p] = yv;  // 0 for c >= k
+          if (q == 0) Wsm[r][p] = yv;  // 0 for c >= k
           const int64_t row = b * T + tcur;
           if (blog && lane == 0) blog[row] = 1;
           if (clog && lane < R) clog[row * R + lane] = (lane == r) ? 1.0 : 0.0;
@@ -448,37 +455,29 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
       };
 
       // ---- panel mode --------------------------------------------------------------
-      int64_t staged = -1;
-      auto stage = [&](int64_t t0) {  // rows t0 + 8w + p of warp w's tile
-        const int64_t t = t0 + 8 * w + p;
-        const bool ok = t < T;
-        const TI* src = ok ? Rb + t * M : Rb;
-#pragma unroll
-        for (int jt = 0; jt < NJ; ++jt) cp_async_pair<TI>(&S.At[w][jt][lane][0], src + 8 * jt + 2 * q, ok);
-        cp_commit();
-      };
       while (!stopped && tcur < T) {
         const int64_t t0 = tcur;
-        if (staged != t0) {
-          cp_wait<0>();
-          stage(t0);
-        }
-        cp_wait<0>();
-        PPROBE(2);
         double acc[NJ][2];
+        {
+          // straight from global into the fragment registers; the next panel's
+          // rows are pulled into L2 meanwhile
+          const int64_t t = t0 + 8 * w + p;
+          const bool ok = t < T;
+          const TI* src = Rb + (ok ? t : 0) * M;
 #pragma unroll
-        for (int jt = 0; jt < NJ; ++jt) {
-          const double2 v = slot(&S.At[w][jt][lane][0], 0);
-          acc[jt][0] = v.x;
-          acc[jt][1] = v.y;
+          for (int jt = 0; jt < NJ; ++jt) {
+            const double2 v = ok ? ld2(src + 8 * jt + 2 * q) : make_double2(0.0, 0.0);
+            acc[jt][0] = v.x;
+            acc[jt][1] = v.y;
+          }
+          const int64_t tn = t + PNL;
+          if (tn < T) {
+            const char* nb = reinterpret_cast<const char*>(Rb + tn * M);
+            constexpr int LINES = (int)(M * sizeof(TI) / 128);
+            for (int l = q; l < LINES; l += 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(nb + 128 * l));
+          }
         }
-        // the next panel streams in while this one is projected (own lane slots only)
-        if (t0 + PNL < T) {
-          stage(t0 + PNL);
-          staged = t0 + PNL;
-        } else {
-          staged = -1;
-        }
+        PPROBE(2);
         const int64_t tb = t0 + 8 * w;  // first row of this warp's tile
         const int tv = (int)(T - tb < 0 ? 0 : (T - tb < TT ? T - tb : TT));
         double yv[2];
@@ -573,7 +572,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
         if (w == 0 && lane == 0) {
           S.sGrow = grow ? 1 : 0;
           S.sEnd = 0;
-          S.sR0 = r;
         }
         if (grow && w == ws) {
           // W's new row: y - a.x0 of the growth row (lanes c = p, t = 2q + e)
@@ -640,7 +638,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
         bar_sync_n(BAR_PROJ, PW * 32);  // every column of C~ / C is updated
         PPROBE(6);
       }
-      cp_wait<0>();
       if (!stopped) consumed = T;
       // end-of-stream marker
       bar_sync_n(BAR_EMPTY, PANEL_THREADS);
@@ -648,7 +645,6 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
       if (w == 0 && lane == 0) {
         S.sGrow = 0;
         S.sEnd = 1;
-        S.sR0 = r;
       }
       bar_arrive_n(BAR_FULL, PANEL_THREADS);
     } else {
@@ -667,32 +663,28 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
         }
       }
       int rh = r;
-      bool first = true;
+      if (fresh) {
+        // the row-mode phase grew the basis to r rows: P^-1 = I (solver.py:368-380)
+#pragma unroll
+        for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
+              Pr[mt][nt][e] = (i == i2 && i < rh) ? 1.0 : 0.0;
+            }
+      }
+      // W's rows of the row-mode phase (zero for a continuation call)
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) Wt[mt][e] = Wsm[8 * mt + 2 * q + e][p];
       bar_arrive_n(BAR_EMPTY, PANEL_THREADS);
       while (true) {
         PPROBE(10);
         bar_sync_n(BAR_FULL, PANEL_THREADS);
         PPROBE(9);
-        if (first) {
-          // the row-mode phase grew the basis to sR0 rows: P^-1 = I, W from shared memory
-          first = false;
-          if (fresh) {
-            rh = S.sR0;
-#pragma unroll
-            for (int mt = 0; mt < IT; ++mt)
-#pragma unroll
-              for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int i = 8 * mt + p, i2 = 8 * nt + 2 * q + e;
-                  Pr[mt][nt][e] = (i == i2 && i < rh) ? 1.0 : 0.0;
-                }
-          }
-#pragma unroll
-          for (int mt = 0; mt < IT; ++mt)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) Wt[mt][e] = S.Wsm[8 * mt + 2 * q + e][p];
-        }
         const int nti = (rh + 7) >> 3;
 #pragma unroll 1
         for (int u = 0; u < PW; ++u) {
@@ -808,7 +800,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
           *reinterpret_cast<double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q) =
               make_double2(Pr[mt][nt][0], Pr[mt][nt][1]);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) S.Wsm[8 * mt + 2 * q + e][p] = Wt[mt][e];
+        for (int e = 0; e < 2; ++e) Wsm[8 * mt + 2 * q + e][p] = Wt[mt][e];
       }
     }
     PPROBE(home ? 11 : 7);
@@ -832,7 +824,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, 2) panel_kernel(
 #pragma unroll
         for (int kt = 0; kt < IK; ++kt) {
           const int i = sigma(kt, q);
-          mma(acc, S.Wsm[i][p], S.Df[i >> 3][ksj][4 * (i & 7) + qj]);
+          mma(acc, Wsm[i][p], S.Df[i >> 3][ksj][4 * (i & 7) + qj]);
         }
         if (p < k) *reinterpret_cast<double2*>(Xg + p * M + 8 * jt + 2 * q) = make_double2(acc[0], acc[1]);
       }
