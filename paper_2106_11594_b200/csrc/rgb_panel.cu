@@ -380,9 +380,9 @@ __global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
       while (tcur < T && r < R) {
         const int nt_rt = (r + 7) >> 3;
         bool go;
-        if (nt_rt <= 1) go = row_step(std::integral_constant<int, 1>{});
-        else if (nt_rt == 2) go = row_step(std::integral_constant<int, (2 < IT ? 2 : IT)>{});
-        else if (nt_rt == 3) go = row_step(std::integral_constant<int, (3 < IT ? 3 : IT)>{});
+        // two instantiations, not one per tile count: with three CTAs per SM in
+        // different phases the instruction cache is the next limit (measured)
+        if (nt_rt <= 2) go = row_step(std::integral_constant<int, (2 < IT ? 2 : IT)>{});
         else go = row_step(std::integral_constant<int, IT>{});
         if (!go) break;
       }
