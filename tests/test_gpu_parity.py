@@ -1033,3 +1033,47 @@ def test_warp_group_kernel_other_instantiations(m, r_cap, variant, no_panel, mon
     assert np.array_equal(res["rank"][ok], o["rank"][ok])
     X = oracle.solution(o)
     assert max(relerr(res["x"][b], X[b]) for b in np.nonzero(ok)[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("r_cap", [32, 16])
+def test_panel_kernel_edge_cases(r_cap):
+    """The panel kernel (m 128, general variant) on what config 3 rarely exercises:
+    k = 8 right-hand sides, row counts around the 24-row panel (1, 23, 24, 25),
+    continuation calls whose rows grow the basis in panel mode (x0 != 0, so no
+    row mode), a non-finite row in the middle of a panel, and a stream that runs
+    into r_cap mid-panel -- each against the oracle."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    m, k, n = 128, 8, 97
+    ranks = [3, r_cap - 2, r_cap, r_cap + 5]  # the last one exceeds the capacity
+    rows = np.concatenate([_lowrank_streams(1, n, m, rr, k, seed=40 + i)[0] for i, rr in enumerate(ranks)])
+    tg = np.random.default_rng(7).standard_normal((len(ranks), n, k))
+    rows[1, 50, 17] = np.nan  # stream 1 freezes at row 50 (mid-panel)
+    B = rows.shape[0]
+    o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=8)
+    X = oracle.solution(o)
+    for splits in ([97], [1, 23, 24, 25, 24], [10, 87]):
+        bs = BatchedSolver(B, m, k=k, r_cap=r_cap)
+        br = torch.zeros((B, n), dtype=torch.uint8, device="cuda")
+        lo = 0
+        for cnt in splits:
+            hi = lo + cnt
+            sub = torch.zeros((B, cnt), dtype=torch.uint8, device="cuda")
+            bs.ingest(dev(np.ascontiguousarray(rows[:, lo:hi])), dev(np.ascontiguousarray(tg[:, lo:hi])),
+                      branch_log=sub)
+            br[:, lo:hi] = sub
+            lo = hi
+        torch.cuda.synchronize()
+        st = bs.status.cpu().numpy()
+        rk = bs.rank.cpu().numpy()
+        nobs = bs.nobs_t.cpu().numpy()
+        assert st[1] & 2 and int(nobs[1]) == 50, (splits, st, nobs)
+        assert st[3] & 1 and rk[3] == r_cap, (splits, st, rk)
+        for b in (0, 2):
+            assert st[b] == 0 and rk[b] == o["rank"][b], (splits, b)
+            assert np.array_equal(br[b].cpu().numpy(), o["branch"][b]), (splits, b)
+            assert relerr(bs.solution.cpu().numpy()[b], X[b]) <= 1e-9, (splits, b)
+        # the frozen stream holds the state after its last good row
+        o1 = oracle.ingest(rows[1:2, :50], tg[1:2, :50], r_cap=r_cap)
+        assert rk[1] == o1["rank"][0]
+        assert relerr(bs.solution.cpu().numpy()[1], oracle.solution(o1)[0]) <= 1e-9
