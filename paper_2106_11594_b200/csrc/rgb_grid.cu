@@ -689,8 +689,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
 
 }  // namespace grd
 
-// Workspace pool of the current device: created once, never trimmed.
-static cudaMemPool_t workspace_pool() {
+// Workspace pool of the current device: created once, never trimmed (the grid
+// kernel's workspace, the panel kernel's stream counter).
+cudaMemPool_t workspace_pool() {
   static std::mutex mu;
   static cudaMemPool_t pools[64] = {};
   int dev = 0;

@@ -38,8 +38,9 @@
 // streams, twelve warps) per SM: 74 KB of shared memory and at most 168
 // registers per thread; W's rows share the hand-off slot's memory (the home
 // warp reads them before the first panel and writes W there after the last).
-// Config 3: 2.35 ms against 3.11 ms for the warp-group kernel (2.60 ms with two
-// CTAs per SM and a cp.async stage per warp).  Per stream (scripts/probe_panel.py,
+// Streams are claimed dynamically (an atomic counter).  Config 3: 2.25 ms against
+// 3.11 ms for the warp-group kernel (2.60 ms with two CTAs per SM and a cp.async
+// stage per warp, 2.32 ms with a static round robin).  Per stream (scripts/probe_panel.py,
 // -DRGB_PANEL_PROBE) the row mode is ~1/3 of the time, and the home warp's chain
 // (8x8 LDL^T ~1 900 cycles per tile behind the projection warps' DMMAs) bounds
 // the panel phase.
@@ -139,6 +140,7 @@ struct PanelSmem {
   double sWnew[8];             // growth: W's new row (per RHS)
   int sTe[PW];                 // dependent rows [0, te) of each tile
   int sGrow, sEnd;             // growth marker, end of stream
+  unsigned claim;              // the stream this CTA works on
   // projection-warp exchange
   int stop[PW];                // first stop row of each tile (TT = none)
   int bad[PW];                 // ... and whether it is non-finite
@@ -152,7 +154,7 @@ template <int R, int M, typename TI>
 __global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
     const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
-    double* __restrict__ clog) {
+    double* __restrict__ clog, unsigned* __restrict__ next_stream) {
   using SMT = PanelSmem<R, M, TI>;
   constexpr int IT = SMT::IT, IK = SMT::IK, NJ = SMT::NJ, KS = SMT::KS;
   // own columns of a projection warp (row mode, growth, write-back): the 8-column
@@ -180,7 +182,14 @@ __global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
   }
 #endif
 
-  for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
+  // streams are claimed dynamically (their cost varies with the rank they reach:
+  // row-mode length, rank tiles of every projection and of the P^-1 chain)
+  for (;;) {
+    __syncthreads();  // every thread has read the previous claim
+    if (threadIdx.x == 0) S.claim = atomicAdd(next_stream, 1u);
+    __syncthreads();
+    const int64_t b = S.claim;
+    if (b >= cfg.num_streams) break;
     int status = st.status[b];
     if (status) continue;  // uniform across the block
     int r = st.rank[b];
@@ -857,6 +866,8 @@ __global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
 
 }  // namespace blk
 
+cudaMemPool_t workspace_pool();  // rgb_grid.cu
+
 template <int R, int M, typename TI>
 static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                           const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
@@ -873,10 +884,17 @@ static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > cfg.num_streams) grid = cfg.num_streams;
+  // the stream counter: 4 bytes, stream-ordered, from the library's device pool
+  void* ws = nullptr;
+  cudaMemPool_t pool = workspace_pool();
+  if (!pool || cudaMallocFromPoolAsync(&ws, 256, pool, stream) != cudaSuccess) return RGB_E_CUDA;
+  cudaMemsetAsync(ws, 0, sizeof(unsigned), stream);
   kern<<<(unsigned)grid, blk::PANEL_THREADS, smem, stream>>>(cfg, st, (const TI*)rows, rows_stride,
                                                              (const TI*)targets, tg_stride, T, logs.branch,
-                                                             (double*)logs.coords);
-  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+                                                             (double*)logs.coords, (unsigned*)ws);
+  const cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(ws, stream);
+  return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
 bool panel_supports(const rgb_config& cfg) {
