@@ -184,9 +184,11 @@ __global__ void __launch_bounds__(PANEL_THREADS, 3) panel_kernel(
 
   // streams are claimed dynamically (their cost varies with the rank they reach:
   // row-mode length, rank tiles of every projection and of the P^-1 chain)
-  for (;;) {
+  // (no counter when every CTA has at most one stream: the CTA index is the stream)
+  for (unsigned iter = 0;; ++iter) {
     __syncthreads();  // every thread has read the previous claim
-    if (threadIdx.x == 0) S.claim = atomicAdd(next_stream, 1u);
+    if (threadIdx.x == 0)
+      S.claim = next_stream ? atomicAdd(next_stream, 1u) : (iter == 0 ? blockIdx.x : 0xffffffffu);
     __syncthreads();
     const int64_t b = S.claim;
     if (b >= cfg.num_streams) break;
@@ -885,15 +887,18 @@ static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows
   int64_t grid = (int64_t)num_sms * per_sm;
   if (grid > cfg.num_streams) grid = cfg.num_streams;
   // the stream counter: 4 bytes, stream-ordered, from the library's device pool
+  // (not needed when every CTA gets at most one stream, e.g. a drop-in update())
   void* ws = nullptr;
-  cudaMemPool_t pool = workspace_pool();
-  if (!pool || cudaMallocFromPoolAsync(&ws, 256, pool, stream) != cudaSuccess) return RGB_E_CUDA;
-  cudaMemsetAsync(ws, 0, sizeof(unsigned), stream);
+  if (cfg.num_streams > grid) {
+    cudaMemPool_t pool = workspace_pool();
+    if (!pool || cudaMallocFromPoolAsync(&ws, 256, pool, stream) != cudaSuccess) return RGB_E_CUDA;
+    cudaMemsetAsync(ws, 0, sizeof(unsigned), stream);
+  }
   kern<<<(unsigned)grid, blk::PANEL_THREADS, smem, stream>>>(cfg, st, (const TI*)rows, rows_stride,
                                                              (const TI*)targets, tg_stride, T, logs.branch,
                                                              (double*)logs.coords, (unsigned*)ws);
   const cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(ws, stream);
+  if (ws) cudaFreeAsync(ws, stream);
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 

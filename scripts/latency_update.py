@@ -8,7 +8,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2106_11594_b200 as p  # noqa: E402
 
-for m in (16, 64, 256, 1024):
+for m in [int(v) for v in os.environ.get("RGB_LAT_M", "16,64,256,1024").split(",")]:
     rng = np.random.default_rng(0)
     A = rng.standard_normal((40, m))
     r = min(20, m)
