@@ -107,7 +107,7 @@ int rgb_state_reset(const rgb_config *cfg, rgb_state *state, void *stream);
  * is reset + ingest.  Branch decisions use the reference's rank test
  * (solver.py:292-296).  Streams whose status is nonzero are skipped.  The kernel
  * is chosen from the shape (rgb_abi.cu); the environment variable RGB_NO_PANEL=1
- * turns off the m = 128 panel kernel (A/B runs and tests; results agree within
+ * turns off the panel kernel (m 128 / 256; A/B runs and tests; results agree within
  * the fp64 parity bar, not bitwise, since the summation orders differ). */
 int rgb_ingest(const rgb_config *cfg, rgb_state *state, const void *rows, int64_t rows_stride,
                const void *targets, int64_t targets_stride, int64_t T, const rgb_logs *logs,

@@ -3,9 +3,9 @@
 // Validation mirrors the reference's constructor and input checks
 // (solver.py:142-158, scalars.py:108-138) as return codes.  Dispatch, first
 // match wins: the one-warp tensor-core kernel (m 64, r_cap 16, k <= 8), the
-// panel kernel (m 128, r_cap 16 / 32, general variant; RGB_NO_PANEL=1 in the
-// environment turns it off, for A/B runs and tests), the warp-group kernel
-// (m 128 / r_cap 32, m 256 / r_cap 16, every variant), the cluster kernel
+// panel kernel (general variant: m 128 with r_cap 16 / 32, m 256 with r_cap 16;
+// RGB_NO_PANEL=1 in the environment turns it off, for A/B runs and tests), the
+// warp-group kernel (m 128 / 256 with r_cap 16 / 32, every variant), the cluster kernel
 // (r_cap 64, m <= 1 080) and the grid kernel (a few large streams, m <= 2 368,
 // r_cap <= 512) -- the last two for calls of 8+ rows -- and the shape-generic
 // kernel for everything else, for fp32 state and for per-row residual logs.
