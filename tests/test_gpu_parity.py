@@ -1006,7 +1006,7 @@ def test_random_shapes_against_oracle(seed):
             assert relerr(X[b], XO[b]) <= 1e-9, case
 
 
-@pytest.mark.parametrize("m,r_cap", [(128, 16), (256, 32)])
+@pytest.mark.parametrize("m,r_cap", [(128, 16), (256, 32), (256, 16)])
 @pytest.mark.parametrize("variant", ["general", "orthonormal"])
 @pytest.mark.parametrize("no_panel", [False, True])
 def test_warp_group_kernel_other_instantiations(m, r_cap, variant, no_panel, monkeypatch):
@@ -1016,8 +1016,8 @@ def test_warp_group_kernel_other_instantiations(m, r_cap, variant, no_panel, mon
     from paper_2106_11594_b200.batched import BatchedSolver
 
     if no_panel:
-        if m != 128 or variant != "general":
-            pytest.skip("the panel kernel serves only the general variant at m = 128")
+        if (m, r_cap) not in ((128, 16), (128, 32), (256, 16)) or variant != "general":
+            pytest.skip("the panel kernel serves the general variant at m 128 and at m 256 / r_cap 16")
         monkeypatch.setenv("RGB_NO_PANEL", "1")
 
     B, n = 24, 200
