@@ -71,7 +71,7 @@ struct HomeSmem {
   double slotN[2][MAXCL][2][TT]; //       its norm partials
   double Ps[R][PS];              // P^-1
   double Wb[R][8];               // W (x = x0 + C~^T W)
-  double Ub[R][8], Yb[R][8];
+  double Ub[R][8];
   double Eb[8][8], Dy[8][8];
   double rd[8];
   double zg[R + 8];              // |rej_t|^2 of the rank test; non-general growth: z = P gamma, gamma^T W
@@ -567,39 +567,43 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         }
         __syncthreads();
         PROBE(11);
-        // Y = U E^T (M = i, N = t, K = t'), W += Y (D^-1 E dy0) (M = i, N = cc, K = t)
+        // Y = U E^T: every warp forms all the Y rows its P update needs, directly in
+        // the B-operand layout (the N index of the MMA permuted, n -> t = (n >> 1) +
+        // 4 (n & 1)), so Y needs no exchange through shared memory and no barrier;
+        // then W += Y (D^-1 E dy0) and P -= Y D^-1 Y^T on the own row block
         if (8 * w < r) {
-          double yb[2] = {0.0, 0.0};
+          const int pe = (p >> 1) + 4 * (p & 1);
+          double ya[IT][2], yo[2] = {0.0, 0.0};
 #pragma unroll
-          for (int kt = 0; kt < 2; ++kt) mma(yb, H.Ub[8 * w + p][4 * kt + q], H.Eb[p][4 * kt + q]);
-          H.Yb[8 * w + p][2 * q] = yb[0];
-          H.Yb[8 * w + p][2 * q + 1] = yb[1];
-          __syncwarp();
+          for (int nt = 0; nt < IT; ++nt) {
+            ya[nt][0] = ya[nt][1] = 0.0;
+            if (8 * nt < r) {
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) mma(ya[nt], H.Ub[8 * nt + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
+            }
+          }
+#pragma unroll
+          for (int kt = 0; kt < 2; ++kt) mma(yo, H.Ub[8 * w + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
+          // yo[e] = Y[8w + p][q + 4e]: W's own rows (M = i, N = cc, K = t)
           double wb[2] = {H.Wb[8 * w + p][2 * q], H.Wb[8 * w + p][2 * q + 1]};
 #pragma unroll
-          for (int kt = 0; kt < 2; ++kt) mma(wb, H.Yb[8 * w + p][4 * kt + q], H.Dy[4 * kt + q][p]);
+          for (int kt = 0; kt < 2; ++kt) mma(wb, yo[kt], H.Dy[4 * kt + q][p]);
           H.Wb[8 * w + p][2 * q] = wb[0];
           H.Wb[8 * w + p][2 * q + 1] = wb[1];
-        }
-        __syncthreads();
-        PROBE(12);
-        // P -= Y D^-1 Y^T (M = i, N = i', K = t): warp w owns row block w
-        if (8 * w < r) {
-          const double ys0 = -H.Yb[8 * w + p][q] * H.rd[q], ys1 = -H.Yb[8 * w + p][4 + q] * H.rd[4 + q];
-          double acc[IT][2], y0[IT], y1[IT];
+          // P -= Y D^-1 Y^T (M = i, N = i', K = t): warp w owns row block w
+          const double ys0 = -yo[0] * H.rd[q], ys1 = -yo[1] * H.rd[4 + q];
+          double acc[IT][2];
 #pragma unroll
           for (int nt = 0; nt < IT; ++nt) {
             const double2 v = *reinterpret_cast<const double2*>(&H.Ps[8 * w + p][8 * nt + 2 * q]);
             acc[nt][0] = v.x;
             acc[nt][1] = v.y;
-            y0[nt] = H.Yb[8 * nt + p][q];
-            y1[nt] = H.Yb[8 * nt + p][4 + q];
           }
 #pragma unroll
           for (int nt = 0; nt < IT; ++nt) {
             if (8 * nt < r) {
-              mma(acc[nt], ys0, y0[nt]);
-              mma(acc[nt], ys1, y1[nt]);
+              mma(acc[nt], ys0, ya[nt][0]);
+              mma(acc[nt], ys1, ya[nt][1]);
             }
           }
 #pragma unroll
@@ -607,6 +611,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
             if (8 * nt < r)
               *reinterpret_cast<double2*>(&H.Ps[8 * w + p][8 * nt + 2 * q]) = make_double2(acc[nt][0], acc[nt][1]);
         }
+        PROBE(12);
         if (tid < 8 && base + tid >= rs && base + tid < te) {  // logs of the dependent rows
           const int64_t row = b * T + t0 + base + tid;
           if (blog) blog[row] = 0;
