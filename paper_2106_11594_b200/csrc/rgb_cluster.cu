@@ -295,8 +295,14 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
             const int e0 = c * chunk, e1 = (e0 + chunk < NE) ? e0 + chunk : NE;
             double(*hg)[HGS] = rem(ncol)->u.home.slotG[j];
             for (int e = e0 + tid; e < e1; e += NT) {
+              // every remote load in flight before the fixed-order sum
+              double pv[MAXCL];
+#pragma unroll
+              for (int u = 0; u < MAXCL; ++u) pv[u] = (u < ncol) ? rem(u)->u.col.Gp[e] : 0.0;
               double v = 0.0;
-              for (int u = 0; u < ncol; ++u) v += rem(u)->u.col.Gp[e];
+#pragma unroll
+              for (int u = 0; u < MAXCL; ++u)
+                if (u < ncol) v += pv[u];
               const int t = e / GX, i = e % GX;
               for (int u = 0; u < ncol; ++u) rem(u)->u.col.Gs[t][i] = v;
               hg[t][i] = v;
