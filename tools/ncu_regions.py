@@ -50,7 +50,8 @@ def line_map(so, kernel_sub, fname, ninstr):
                 # outermost occurrence of the file in this line-info record (caller side)
                 ms = re.findall(r'File "[^"]*' + re.escape(fname) + r'", line (\d+)', ln)
                 if ms:
-                    cur = int(ms[-1])
+                    # outermost by default; RGB_NCU_INNER=1: the innermost line of this file
+                    cur = int(ms[0] if os.environ.get("RGB_NCU_INNER") else ms[-1])
                 continue
             m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
             if m and func is not None:
