@@ -34,18 +34,18 @@
 //    shared memory.
 //
 // General variant, fp64 state, k <= 8 right-hand sides, float64 or float32
-// inputs; instantiated for m = 128 with r_cap 16 and 32, and for m = 256 with
-// r_cap 16 (config 1: one CTA per SM, 254 registers; 0.099 ms per solve against
-// 0.143 ms on the warp-group kernel).  Three CTAs (three
-// streams, twelve warps) per SM: 74 KB of shared memory and at most 168
-// registers per thread; W's rows share the hand-off slot's memory (the home
-// warp reads them before the first panel and writes W there after the last).
-// Streams are claimed dynamically (an atomic counter).  Config 3: 2.25 ms against
-// 3.11 ms for the warp-group kernel (2.60 ms with two CTAs per SM and a cp.async
-// stage per warp, 2.32 ms with a static round robin).  Per stream (scripts/probe_panel.py,
+// inputs; instantiated for m = 128 with r_cap 16 and 32 (three CTAs -- three
+// streams, twelve warps -- per SM: 74 KB of shared memory, at most 168 registers
+// per thread) and for m = 256 with r_cap 16 (config 1: one CTA per SM, 254
+// registers; 0.099 ms per solve against 0.143 ms on the warp-group kernel).  W's
+// rows share the hand-off slot's memory (the home warp reads them before the
+// first panel and writes W there after the last).  Streams are claimed
+// dynamically (an atomic counter).  Config 3: 2.22 ms against 3.11 ms for the
+// warp-group kernel (2.60 ms with two CTAs per SM and a cp.async stage per warp,
+// 2.32 ms with a static round robin).  Per stream (scripts/probe_panel.py,
 // -DRGB_PANEL_PROBE) the row mode is ~1/3 of the time, and the home warp's chain
 // (8x8 LDL^T ~1 900 cycles per tile behind the projection warps' DMMAs) bounds
-// the panel phase.
+// the panel phase; DESIGN.md lists the variants measured and rejected.
 //
 // Fragment layouts (lane = 4p + q; sigma(kt,q) = 8(kt>>1) + 2q + (kt&1)):
 //   tile   acc[jt][e]        = A[t=p][8jt+2q+e]         registers (A- and B-operand, K = sigma)
