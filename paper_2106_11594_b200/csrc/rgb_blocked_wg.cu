@@ -740,11 +740,8 @@ static int launch_wg(const rgb_config& cfg, rgb_state& st, const void* rows, int
   const bool gen = cfg.variant == RGB_GENERAL;
   auto kern = gen ? blk::blocked_wg_kernel<R, WG, true, TI> : blk::blocked_wg_kernel<R, WG, false, TI>;
   const size_t smem = sizeof(blk::GroupSmem<R, WG, TI>);
-  static bool attr[2] = {false, false};
-  if (!attr[gen]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[gen] = true;
-  }
+  static bool attr[2][64] = {};
+  smem_attr_once(kern, smem, attr[gen]);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WG * 32, smem);
   if (per_sm < 1) per_sm = 1;

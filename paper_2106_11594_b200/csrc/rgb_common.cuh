@@ -42,6 +42,23 @@ __device__ __forceinline__ bool is_dependent(REAL rej_sq, REAL row_sq, REAL esq)
   return (rej_sq < esq) || (rej_sq < esq * row_sq);
 }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per device
+// (the attribute belongs to the device's context, so a per-process flag would
+// skip every device after the first).  Setting it twice from racing host
+// threads is harmless.
+template <typename K>
+inline void smem_attr_once(K kern, size_t smem, bool (&done)[64]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return;
+  }
+  if (!done[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    done[dev] = true;
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -878,11 +878,8 @@ static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows
                           cudaStream_t stream, int num_sms) {
   auto kern = blk::panel_kernel<R, M, TI>;
   const size_t smem = sizeof(blk::PanelSmem<R, M, TI>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  static bool attr[64] = {};
+  smem_attr_once(kern, smem, attr);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, blk::PANEL_THREADS, smem);
   if (per_sm < 1) per_sm = 1;
