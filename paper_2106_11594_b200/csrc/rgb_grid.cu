@@ -19,8 +19,10 @@
 //       Y_b = U_b E^T -> ws; W_b += Y_b D^-1 E dy0
 //   P6  P_b -= Y_b D^-1 Y^T  (overlaps P1 of the next tile)
 //
-// five grid barriers per 8 rows instead of three-plus per row for a per-row
-// multi-SM scheme.  An independent row (solver.py:305-318) is applied by
+// four grid barriers per 8 rows (U_b and the S / G W partials of P4 are formed
+// in P3 for every row of the tile and masked after the rank test, which leaves
+// the values of the masked computation unchanged) instead of three-plus per row
+// for a per-row multi-SM scheme.  An independent row (solver.py:305-318) is applied by
 // every CTA to its own columns / row block, and the rest of its tile is
 // re-projected.  The workspace (partials, barrier counter) is allocated per
 // call, stream-ordered on the caller's stream, so calls stay reentrant; it
@@ -328,6 +330,39 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             ws_r[((size_t)0 * TT + tid) * nc + c] = s;
           }
         }
+        // U_b = P_b G^T and the S / G W partials of every row of the tile, before the
+        // rank test is known: the rows the test leaves out are masked afterwards
+        // (zeroing the rows / columns of S and the columns of U_b gives the values of
+        // the masked computation exactly), which saves the grid barrier that used to
+        // separate the test from these partials
+        if (owner) {
+          // U_b = P_b G^T (M = i in my block, N = t, K = i' split over warps)
+          double acc[2] = {0.0, 0.0};
+          for (int kt = w; kt < R / 4; kt += NW) mma(acc, S.Ps[p][4 * kt + q], S.Gs[p][4 * kt + q]);
+          __syncthreads();  // S.red is free again (the R reduction above is done)
+          S.red[w][p * 8 + 2 * q] = acc[0];
+          S.red[w][p * 8 + 2 * q + 1] = acc[1];
+          __syncthreads();
+          if (tid < 64) {
+            double v = 0.0;
+#pragma unroll
+            for (int u = 0; u < NW; ++u) v += S.red[u][tid];
+            S.Ub[tid >> 3][tid & 7] = v;
+          }
+          __syncthreads();
+          if (w == 0) {
+            // S_b = G[:, b] U_b and (G W)_b = G[:, b] W_b (M = t, K = i in my block)
+            double sp[2] = {0.0, 0.0}, gw[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt) {
+              const double a = S.Gs[p][8 * c + 4 * kt + q];
+              mma(sp, a, S.Ub[4 * kt + q][p]);
+              mma(gw, a, S.Wb[4 * kt + q][p]);
+            }
+            *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2) * 64 + p * 8 + 2 * q) = make_double2(sp[0], sp[1]);
+            *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2 + 1) * 64 + p * 8 + 2 * q) = make_double2(gw[0], gw[1]);
+          }
+        }
         GPROBE(4);
         grid_sync(ctr, epoch);
         GPROBE(5);
@@ -380,39 +415,6 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           // ---- dependent rows [row_start, tstar): blocked Sherman-Morrison
           const int rs = row_start, te = tstar;
           if (owner) {
-            // U_b = P_b G^T (M = i in my block, N = t, K = i' split over warps)
-            double acc[2] = {0.0, 0.0};
-            const bool in_t = p >= rs && p < te;  // B operand column t = p
-            for (int kt = w; kt < R / 4; kt += NW)
-              mma(acc, S.Ps[p][4 * kt + q], in_t ? S.Gs[p][4 * kt + q] : 0.0);
-            S.red[w][p * 8 + 2 * q] = acc[0];
-            S.red[w][p * 8 + 2 * q + 1] = acc[1];
-            __syncthreads();
-            if (tid < 64) {
-              double v = 0.0;
-#pragma unroll
-              for (int u = 0; u < NW; ++u) v += S.red[u][tid];
-              S.Ub[tid >> 3][tid & 7] = v;
-            }
-            __syncthreads();
-            if (w == 0) {
-              // S_b = G[:, b] U_b and (G W)_b = G[:, b] W_b (M = t, K = i in my block)
-              const bool in_r = p >= rs && p < te;
-              double sp[2] = {0.0, 0.0}, gw[2] = {0.0, 0.0};
-#pragma unroll
-              for (int kt = 0; kt < 2; ++kt) {
-                const double a = in_r ? S.Gs[p][8 * c + 4 * kt + q] : 0.0;
-                mma(sp, a, S.Ub[4 * kt + q][p]);
-                mma(gw, a, S.Wb[4 * kt + q][p]);
-              }
-              *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2) * 64 + p * 8 + 2 * q) = make_double2(sp[0], sp[1]);
-              *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2 + 1) * 64 + p * 8 + 2 * q) = make_double2(gw[0], gw[1]);
-            }
-          }
-          GPROBE(6);
-          grid_sync(ctr, epoch);
-          GPROBE(7);
-          if (owner) {
             {
               // sums of the S and G W partials: warp w takes owners w, w+8, ...
               double a4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -447,9 +449,13 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
                 gws[0] += S.red[u][4 * lane + 2];
                 gws[1] += S.red[u][4 * lane + 3];
               }
+              const bool in_r = p >= rs && p < te;
+              // rows / columns outside the dependent rows [rs, te) drop out of S
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (!in_r || 2 * q + e < rs || 2 * q + e >= te) mi[e] = 0.0;
               if (p == 2 * q) mi[0] += 1.0;
               if (p == 2 * q + 1) mi[1] += 1.0;
-              const bool in_r = p >= rs && p < te;
 #pragma unroll
               for (int e = 0; e < 2; ++e)  // dy0[t = p][cc = 2q + e]
                 S.Dy[p][2 * q + e] = in_r ? S.Yv[p][2 * q + e] - S.Gs[p][R + 2 * q + e] - gws[e] : 0.0;
@@ -472,6 +478,11 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               S.Eb[p][2 * q] = ev[0];
               S.Eb[p][2 * q + 1] = ev[1];
               if ((p >> 1) == q) S.rd[p] = rcp64((p & 1) ? mi[1] : mi[0]);
+              __syncwarp();
+              // ... and the columns of U_b
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt)
+                if (4 * kt + q < rs || 4 * kt + q >= te) S.Ub[p][4 * kt + q] = 0.0;
               __syncwarp();
               // Y_b = U_b E^T (M = i, N = t, K = t')
               double yb[2] = {0.0, 0.0};
