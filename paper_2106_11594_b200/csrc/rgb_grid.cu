@@ -19,10 +19,11 @@
 //       Y_b = U_b E^T -> ws; W_b += Y_b D^-1 E dy0
 //   P6  P_b -= Y_b D^-1 Y^T  (overlaps P1 of the next tile)
 //
-// four grid barriers per 8 rows (U_b and the S / G W partials of P4 are formed
+// three grid barriers per 8 rows (U_b and the S / G W partials of P4 are formed
 // in P3 for every row of the tile and masked after the rank test, which leaves
-// the values of the masked computation unchanged) instead of three-plus per row
-// for a per-row multi-SM scheme.  An independent row (solver.py:305-318) is applied by
+// the values of the masked computation unchanged; P6 waits for the next
+// projection's first barrier) instead of three-plus per row for a per-row
+// multi-SM scheme.  An independent row (solver.py:305-318) is applied by
 // every CTA to its own columns / row block, and the rest of its tile is
 // re-projected.  The workspace (partials, barrier counter) is allocated per
 // call, stream-ordered on the caller's stream, so calls stay reentrant; it
@@ -150,6 +151,40 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     int status = st.status[b];
     if (status) continue;
     int r = st.rank[b];
+    // P_b -= Y_b D^-1 Y^T of the last dependent block, deferred to the next grid
+    // barrier (the next projection's P1 barrier, or one of its own before a
+    // non-general growth / the write-back): P is next read by the next tile's U_b,
+    // and a general growth only resets row / column r, which Y leaves untouched
+    bool pending_p6 = false;
+    auto apply_p6 = [&]() {
+        if (owner) {
+          // P_b -= Y_b D^-1 Y^T (M = i in my block, N = i', K = t)
+          const double ys0 = -S.Yb[p][q] * S.rd[q], ys1 = -S.Yb[p][4 + q] * S.rd[4 + q];
+          const int nlive = (r + 7) >> 3;  // row blocks of Y past the rank are zero
+          constexpr int NPW = (IT + NW - 1) / NW;
+          double y0[NPW], y1[NPW];  // every L2 load in flight first
+#pragma unroll
+          for (int i = 0; i < NPW; ++i) {
+            const int nt = w + NW * i;
+            const bool on = nt < nlive;
+            y0[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + q) : 0.0;
+            y1[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + 4 + q) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < NPW; ++i) {
+            const int nt = w + NW * i;
+            if (nt < nlive) {
+              double acc[2] = {S.Ps[p][8 * nt + 2 * q], S.Ps[p][8 * nt + 2 * q + 1]};
+              mma(acc, ys0, y0[i]);
+              mma(acc, ys1, y1[i]);
+              S.Ps[p][8 * nt + 2 * q] = acc[0];
+              S.Ps[p][8 * nt + 2 * q + 1] = acc[1];
+            }
+          }
+        }
+      __syncthreads();
+      pending_p6 = false;
+    };
     const int64_t nobs0 = st.nobs[b];
     double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)rc * M;
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)rc * M;
@@ -236,6 +271,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         GPROBE(0);
         grid_sync(ctr, epoch);
         GPROBE(1);
+        if (pending_p6) apply_p6();
         // ---- P2: G = sum of the partials.  CTA c reduces a contiguous chunk of
         // elements: warp w reads partials u = w, w+8, ... (coalesced rows of
         // 32 elements), then the 8 warp sums are added in a fixed order.
@@ -507,40 +543,13 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               S.Wb[p][2 * q + 1] = wb[1];
             }
           }
-          GPROBE(8);
-          grid_sync(ctr, epoch);
-          GPROBE(9);
-          if (owner) {
-            // P_b -= Y_b D^-1 Y^T (M = i in my block, N = i', K = t)
-            const double ys0 = -S.Yb[p][q] * S.rd[q], ys1 = -S.Yb[p][4 + q] * S.rd[4 + q];
-            const int nlive = (r + 7) >> 3;  // row blocks of Y past the rank are zero
-            constexpr int NPW = (IT + NW - 1) / NW;
-            double y0[NPW], y1[NPW];  // every L2 load in flight first
-#pragma unroll
-            for (int i = 0; i < NPW; ++i) {
-              const int nt = w + NW * i;
-              const bool on = nt < nlive;
-              y0[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + q) : 0.0;
-              y1[i] = on ? __ldcg(ws_y + (size_t)(8 * nt + p) * TT + 4 + q) : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < NPW; ++i) {
-              const int nt = w + NW * i;
-              if (nt < nlive) {
-                double acc[2] = {S.Ps[p][8 * nt + 2 * q], S.Ps[p][8 * nt + 2 * q + 1]};
-                mma(acc, ys0, y0[i]);
-                mma(acc, ys1, y1[i]);
-                S.Ps[p][8 * nt + 2 * q] = acc[0];
-                S.Ps[p][8 * nt + 2 * q + 1] = acc[1];
-              }
-            }
-          }
           if (c == 0 && tid < TT && tid >= rs && tid < te) {
             const int64_t row = b * T + t0 + tid;
             if (blog) blog[row] = 0;
             if (clog)
               for (int i = 0; i < rc; ++i) clog[row * rc + i] = S.Gs[tid][i];
           }
+          pending_p6 = true;  // applied after the next grid barrier (see apply_p6)
           __syncthreads();
         }
         if (tstar >= tv) break;
@@ -589,6 +598,10 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           __syncthreads();
           r += 1;
         } else {
+          if (pending_p6) {  // z = P gamma needs the folded P
+            grid_sync(ctr, epoch);
+            apply_p6();
+          }
           // orthogonal / orthonormal growth: C~[:r] and C[:r] stay, P gains an
           // edge -alpha z and a corner alpha^2 (1 + gamma.z), z = P gamma
           // (solver.py:307-310, 382-395); W gains alpha (y - a.x), a.x = a.x0 + gamma^T W
@@ -663,6 +676,10 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       if (!stopped) consumed = t0 + tv;
     }
 
+    if (pending_p6) {
+      grid_sync(ctr, epoch);
+      apply_p6();
+    }
     // ---- write back: C~, C, P, W -> ws, then x = x0 + C~^T W on my columns ------------
     for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
       const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
