@@ -71,7 +71,7 @@ struct HomeSmem {
   double slotN[2][MAXCL][2][TT]; //       its norm partials
   double Ps[R][PS];              // P^-1
   double Wb[R][8];               // W (x = x0 + C~^T W)
-  double Ub[R][8];
+  double Ub[2][R][8];            // U of the block, double-buffered (no barrier between blocks)
   double Eb[8][8], Dy[8][8];
   double rd[8];
   double zg[R + 8];              // |rej_t|^2 of the rank test; non-general growth: z = P gamma, gamma^T W
@@ -491,7 +491,9 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       // blocked Sherman-Morrison over dependent rows [rs, te) of the 8-row block at
       // panel row base (M = I + G P G^T = L D L^T, E = L^-1; Y = P G^T E^T;
       // P -= Y D^-1 Y^T; W += Y D^-1 E dy0, dy0 = y - a.x0 - G W)
+      unsigned nblk = 0;  // dependent blocks folded (selects the U buffer)
       auto dep_block = [&](int s, const double (*Gs)[HGS], int base, int rs, int te, int64_t t0) {
+        const int ub = (int)(nblk++ & 1u);
         const int kr = (r + 3) >> 2;  // K steps over the rank (rows beyond it are zero)
         const bool in_t = base + p >= rs && base + p < te;
         {  // U = P G^T (M = i, N = t, K = i'): warp w owns rows 8w..8w+7
@@ -507,8 +509,8 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
             for (int kt = 0; kt < IK; ++kt)
               if (kt < kr) mma(acc[kt & 3], a[kt], g[kt]);
           }
-          H.Ub[8 * w + p][2 * q] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
-          H.Ub[8 * w + p][2 * q + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+          H.Ub[ub][8 * w + p][2 * q] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+          H.Ub[ub][8 * w + p][2 * q + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
           __syncwarp();
           // this warp's share of S = G U and G W: K = its own rows i = 8w..8w+7
           double sp[2] = {0.0, 0.0}, gp[2] = {0.0, 0.0};
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
 #pragma unroll
             for (int kt = 0; kt < 2; ++kt) {
               const double a0 = in_t ? Gs[base + p][8 * w + 4 * kt + q] : 0.0;
-              mma(sp, a0, H.Ub[8 * w + 4 * kt + q][p]);
+              mma(sp, a0, H.Ub[ub][8 * w + 4 * kt + q][p]);
               mma(gp, a0, H.Wb[8 * w + 4 * kt + q][p]);
             }
           }
@@ -585,11 +587,11 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
             ya[nt][0] = ya[nt][1] = 0.0;
             if (8 * nt < r) {
 #pragma unroll
-              for (int kt = 0; kt < 2; ++kt) mma(ya[nt], H.Ub[8 * nt + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
+              for (int kt = 0; kt < 2; ++kt) mma(ya[nt], H.Ub[ub][8 * nt + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
             }
           }
 #pragma unroll
-          for (int kt = 0; kt < 2; ++kt) mma(yo, H.Ub[8 * w + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
+          for (int kt = 0; kt < 2; ++kt) mma(yo, H.Ub[ub][8 * w + p][4 * kt + q], H.Eb[pe][4 * kt + q]);
           // yo[e] = Y[8w + p][q + 4e]: W's own rows (M = i, N = cc, K = t)
           double wb[2] = {H.Wb[8 * w + p][2 * q], H.Wb[8 * w + p][2 * q + 1]};
 #pragma unroll
@@ -624,7 +626,8 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           if (clog)
             for (int i = 0; i < rc; ++i) clog[row * rc + i] = Gs[base + tid][i];
         }
-        __syncthreads();
+        // no barrier: the next block reads only its own rows of P^-1 and W, writes
+        // the other U buffer, and its first barrier orders the rest
         PROBE(13);
       };
 
@@ -669,6 +672,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           const double rsq_ts = tstar < tv ? H.zg[tstar] : 0.0;
           __syncthreads();
           for (int base = (row_start & ~7); base < tstar; base += 8) dep_block(s, Gs, base, row_start, tstar, t0);
+          __syncthreads();  // every warp's P^-1 / W rows are folded (growth below writes across blocks)
           bool done = tstar >= tv;
           if (!done && (((badm >> tstar) & 1u) || r >= rc)) {
             status |= ((badm >> tstar) & 1u) ? RGB_ST_NONFINITE : RGB_ST_RANK_CAP;
