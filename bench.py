@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4096)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dump", default=None,
+                    help="rank 0 writes the per-stream ranks / status / x of the untimed pass (npz), for tests")
     args = ap.parse_args()
     if args.eps is None and args.dtype == "fp32":
         # float32 inputs carry ~6e-8 relative rounding: the auto policy's fp64
@@ -205,6 +207,17 @@ def cpu_sample_inputs(cfg_name, count, rows_dev=None, tg_dev=None):
     if rows_dev is not None:
         return rows_dev[:count].cpu().numpy(), tg_dev[:count].cpu().numpy()
     if cfg_name in ("c5", "c3"):
+        try:
+            import torch
+
+            if torch.cuda.is_available():  # the GPU arm's bytes (input generation only, no kernel of ours)
+                r, t = workloads.device_batch(cfg_name, 0, max(count, 2048), "cuda", chunk=2048)
+                out = r[:count].cpu().numpy(), t[:count].cpu().numpy()
+                del r, t
+                torch.cuda.empty_cache()
+                return out
+        except Exception:  # noqa: BLE001  (no usable GPU: regenerate on the host)
+            pass
         from multiprocessing import Pool
 
         with Pool(min(16, os.cpu_count() or 1)) as p:
@@ -244,6 +257,48 @@ def cpu_baseline(cfg_name, dtype, rows, tg, reps=1, eps=None):
 
 # -- reference arm ---------------------------------------------------------------------
 
+def _py_ref_stream(args):
+    """One stream through the reference's own solve_batch (baseline/_ref), one
+    call per right-hand side (the reference has no multi-RHS API)."""
+    rows, tg = args
+    from rankrls import solver as ref_solver
+
+    for c in range(tg.shape[1]):
+        ref_solver.solve_batch(rows, tg[:, c])
+    return rows.shape[0]
+
+
+def python_reference(rows, tg, cores):
+    """The reference package itself (pip-installed into baseline/_ref, the
+    unmodified rankrls 0.1.0 `solve_batch`, general variant, auto eps) on a
+    small sample of the same streams: multiprocessing.Pool(cores), one stream
+    per task, OPENBLAS_NUM_THREADS=1 per worker."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "rankrls")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference/pkg)"}
+    import multiprocessing as mproc
+
+    env_old = os.environ.get("OPENBLAS_NUM_THREADS")
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, ref_dir)
+    try:
+        ctx = mproc.get_context("fork")
+        with ctx.Pool(cores) as pool:
+            pool.map(_py_ref_stream, [(rows[0, :8], tg[0, :8])] * cores)  # warm-up (imports)
+            t0 = time.perf_counter()
+            done = sum(pool.map(_py_ref_stream, [(rows[i], tg[i]) for i in range(rows.shape[0])], chunksize=1))
+            dt = time.perf_counter() - t0
+    finally:
+        sys.path.remove(ref_dir)
+        if env_old is None:
+            os.environ.pop("OPENBLAS_NUM_THREADS", None)
+        else:
+            os.environ["OPENBLAS_NUM_THREADS"] = env_old
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "reference (Python, baseline/_ref)",
+            "sample": f"{rows.shape[0]} streams x {rows.shape[1]} rows, {tg.shape[2] if tg.ndim == 3 else 1} "
+                      f"solve_batch calls per stream (one per RHS), {dt:.2f} s measured"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -257,16 +312,29 @@ def run_reference(args):
     v = statistics.median([c["value"] for c in vals])
     cb = dict(vals[0])
     cb["value"] = v
+    sample_rows = rows.shape[0] * rows.shape[1]
     n_total = cfg.streams * cfg.n
+    py = None
+    if cfg.streams > 1 and args.dtype == "fp64" and args.eps is None:
+        cores = len(os.sched_getaffinity(0))
+        ns = min(len(rows), 8 * cores)
+        py = python_reference(rows[:ns], tg[:ns], cores)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_total / v,
+        "steps": args.steps, "warmup": args.warmup,
+        # each step is the bounded sample, measured; the full-workload time is
+        # an extrapolation at the same per-row rate and is labelled as such
+        "ms_per_step": 1e3 * sample_rows / v,
+        "ms_per_full_workload_extrapolated": 1e3 * n_total / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.dtype == "fp32-state" else "f64", "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d))",
+        "dtype": "f32" if args.dtype == "fp32-state" else "f64",
+        "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d)); the sample's bytes are the GPU arm's device-generated "
+                "streams when a GPU is present",
         "config": {"workload": args.config, "streams": cfg.streams, "streams_per_gpu": cfg.streams, "n": cfg.n,
-                   "m": cfg.m, "k": cfg.k,
-                   "rank": cfg.r, "sampled_streams": rows.shape[0]},
+                   "m": cfg.m, "k": cfg.k, "rank": cfg.r, "sampled_streams": rows.shape[0],
+                   "sampled_rows_per_step": sample_rows},
         "cpu_baseline": cb,
+        "python_reference": py,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -325,6 +393,18 @@ def run_ours(args):
     flops = algorithmic_flops(branch, cfg.m, cfg.k)
     status = bs.status.cpu().numpy()
     ranks = bs.rank.cpu().numpy()
+    # rows actually folded per step (a stream frozen at the rank capacity or on a
+    # non-finite row stops counting observations)
+    nobs_local = int(bs.nobs_t.sum().item())
+    if args.dump:
+        dump = {"rank": sharding.gather_streams(bs.rank_t.cpu(), device).cpu().numpy(),
+                "status": sharding.gather_streams(bs.status_t.cpu(), device).cpu().numpy(),
+                "nobs": sharding.gather_streams(bs.nobs_t.cpu(), device).cpu().numpy(),
+                "x": sharding.gather_streams(bs.x_t.cpu(), device).cpu().numpy(),
+                "branch": sharding.gather_streams(branch.cpu(), device).cpu().numpy()}
+        if rank == 0:
+            np.savez_compressed(args.dump, **dump)
+        del dump
     del branch
 
     def barrier():
@@ -377,7 +457,7 @@ def run_ours(args):
     n_cap = int(sharding.sum_over_ranks(int((status & 1).astype(bool).sum()), device))
     n_nonfinite = int(sharding.sum_over_ranks(int((status & 2).astype(bool).sum()), device))
 
-    total_rows = B * n
+    total_rows = int(sharding.sum_over_ranks(nobs_local, device))
     value = total_rows * args.steps / (elapsed_ms * 1e-3)
 
     # parity spot check outside the timed region: oracle on this rank's first streams
@@ -413,7 +493,7 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, bs, rows, tg, stream, world, local, device, esize)
         ms = sharding.max_over_ranks(e2e.pop("_ms"), device)
-        e2e["value"] = B * n * e2e.pop("_steps") / (ms * 1e-3)
+        e2e["value"] = total_rows * e2e.pop("_steps") / (ms * 1e-3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -529,10 +609,55 @@ def run_e2e(args, bs, rows, tg, stream, world, local, device, esize):
                     if S_e != S else "pinned host -> device copies overlapped with ingest (BatchedSolver.ingest_host)"}
 
 
+# -- process launch -------------------------------------------------------------------
+
+def _free_port():
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n, argv, env=None):
+    """One process per GPU without torchrun: start `argv` n times with RANK /
+    LOCAL_RANK / WORLD_SIZE / MASTER_ADDR / MASTER_PORT set (the same env
+    torchrun gives each rank), wait for all, return the first non-zero exit
+    code.  If one rank fails the others are stopped by PID (a rank stuck in a
+    collective would otherwise wait forever)."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        e = dict(os.environ if env is None else env, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                 LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen(argv, env=e))
+    rc = 0
+    live = list(procs)
+    while live:
+        for p in list(live):
+            code = p.poll()
+            if code is None:
+                continue
+            live.remove(p)
+            if code != 0 and rc == 0:
+                rc = code
+                for q in live:
+                    q.terminate()
+        time.sleep(0.05)
+    return rc
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         return run_reference(args)
+    if world_env is None and args.gpus > 1:
+        # `python bench.py --gpus N`: spawn the N ranks ourselves
+        return launch_ranks(args.gpus, [sys.executable, os.path.abspath(__file__)] + sys.argv[1:])
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; launch one rank per GPU "
+                         "with matching counts")
     return run_ours(args)
 
 

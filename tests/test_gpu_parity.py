@@ -1077,3 +1077,36 @@ def test_panel_kernel_edge_cases(r_cap):
         o1 = oracle.ingest(rows[1:2, :50], tg[1:2, :50], r_cap=r_cap)
         assert rk[1] == o1["rank"][0]
         assert relerr(bs.solution.cpu().numpy()[1], oracle.solution(o1)[0]) <= 1e-9
+
+
+# -- bench.py's multi-rank path (two ranks sharing one B200, gloo) ------------------
+
+def test_bench_two_ranks_equal_one_rank(tmp_path):
+    """`python bench.py --gpus 2` launches its own two ranks (no torchrun); each
+    folds a contiguous half of the global streams with no collective on the
+    data path.  The job reports n_gpus 2 and its per-stream results equal a
+    one-rank run over the same global streams, bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    common = [sys.executable, os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3", "--no-e2e",
+              "--no-cpu", "--dist-backend", "gloo"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    p2 = subprocess.run(common + ["--gpus", "2", "--streams", "2048", "--dump", str(tmp_path / "two.npz")],
+                        env=env, capture_output=True, text=True, timeout=900)
+    assert p2.returncode == 0, p2.stderr[-2000:]
+    line = json.loads(p2.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["streams"] == 4096
+    p1 = subprocess.run(common + ["--gpus", "1", "--streams", "4096", "--dump", str(tmp_path / "one.npz")],
+                        env=env, capture_output=True, text=True, timeout=900)
+    assert p1.returncode == 0, p1.stderr[-2000:]
+    one = json.loads(p1.stdout.strip().splitlines()[-1])
+    assert one["n_gpus"] == 1
+    a, b = np.load(tmp_path / "two.npz"), np.load(tmp_path / "one.npz")
+    for key in ("rank", "status", "nobs", "x", "branch"):
+        assert np.array_equal(a[key], b[key]), key
+    # value counts the rows actually folded (sum of nobs)
+    assert abs(line["value"] * line["ms_per_step"] * 1e-3 - int(a["nobs"].sum())) <= 1e-6 * a["nobs"].sum()
