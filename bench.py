@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-chunk", type=int, default=4096)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--op", default="ingest", choices=["ingest", "pinv", "covariance"],
+                    help="pinv / covariance: time the A+ / covariance extraction (rgb_pinv / rgb_covariance) "
+                         "from the factors of the config's ingested streams instead of the ingest")
     ap.add_argument("--dump", default=None,
                     help="rank 0 writes the per-stream ranks / status / x of the untimed pass (npz), for tests")
     args = ap.parse_args()
@@ -611,6 +614,83 @@ def run_e2e(args, bs, rows, tg, stream, world, local, device, esize):
 
 # -- process launch -------------------------------------------------------------------
 
+# -- extraction (A+ / covariance) ------------------------------------------------------
+
+def run_extract(args):
+    """rgb_pinv / rgb_covariance timed on the device: the config's streams are
+    ingested once (with the coords log, untimed), then each step extracts A+
+    (m x n per stream, PseudoinverseTracker.pinv / pinv_from_scratch,
+    tracking.py:19-85, 128-142) or the covariance (m x m, CovarianceTracker,
+    tracking.py:88-119).  L2 is flushed between steps when the data fits in it."""
+    import torch
+
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    torch.cuda.set_device(0)
+    device = torch.device("cuda", 0)
+    cfg = workloads.CONFIGS[args.config]
+    S = args.streams or cfg.streams
+    if cfg.streams > 1:
+        rows, tg = workloads.device_batch(args.config, 0, S, device)
+    else:
+        A, y = getattr(workloads, args.config)()
+        rows = torch.as_tensor(A[None], device=device)
+        tg = torch.as_tensor(y[None, :, None], device=device)
+    n, m = rows.shape[1], cfg.m
+    bs = BatchedSolver(S, m, k=cfg.k, r_cap=cfg.r_cap, device=device)
+    coords = torch.zeros((S, n, cfg.r_cap), dtype=torch.float64, device=device)
+    bs.ingest(rows, tg, coords_log=coords)
+    torch.cuda.synchronize()
+    del rows, tg
+    ranks = bs.rank.to(torch.float64)
+    ncols = n if args.op == "pinv" else m
+    # algorithmic work (closed form C~^T P^-1 F, F = B^T or C~): the m x r x ncols
+    # contraction plus V = P^-1 C~ (r x r x m), r the stream's rank
+    flops = float((2 * m * ncols * ranks + 2 * ranks * ranks * m).sum().item())
+    # compulsory bytes: the output, the coords log (pinv), C~ and P^-1 at the rank
+    byt = float((8 * (m * ncols + (n * ranks if args.op == "pinv" else 0) + ranks * m + ranks * ranks)).sum().item())
+    run = (lambda: bs.pinv(coords)) if args.op == "pinv" else bs.covariance
+    flush = byt < 2 * 126e6
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=device) if flush else None
+    for _ in range(args.warmup):
+        out = run()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    clocks = ClockSampler(0)
+    clocks.start()
+    for i in range(args.steps):
+        if flush:
+            flush_buf.fill_(float(i))
+        ev[i][0].record()
+        out = run()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    peaks = fp64_peak()
+    mp = measured_peaks()
+    tf = flops / (ms * 1e-3) / 1e12
+    gbs = byt / (ms * 1e-3) / 1e9
+    line = {
+        "metric": f"{args.op} extraction time", "value": ms, "unit": "ms", "higher_is_better": False,
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "dtype": "f64",
+        "data": "synthetic (seeded A = G1 G2, SURVEY.md 8(d))",
+        "config": {"workload": args.config, "op": args.op, "streams": S, "n": n, "m": m, "r_cap": cfg.r_cap,
+                   "output": f"[{S}, {m}, {ncols}] fp64", "l2": "flushed between steps" if flush else "data >> L2"},
+        "roofline": {"bound": "tensor", "achieved": tf, "peak": peaks.get("dmma"), "unit": "TFLOP/s",
+                     "frac": tf / peaks["dmma"] if peaks.get("dmma") else None,
+                     "algorithmic_flops_per_launch": flops,
+                     "hbm": {"achieved_gbs": gbs, "peak_gbs": mp.get("hbm_gbs"),
+                             "frac": gbs / mp["hbm_gbs"] if mp.get("hbm_gbs") else None,
+                             "algorithmic_bytes_per_launch": byt}},
+        "gpu_launches": args.steps * 2,
+        "clocks": clk,
+        "out_checksum": float(out.abs().sum().item()),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def _free_port():
     import socket
 
@@ -658,6 +738,8 @@ def main():
     if world_env is not None and int(world_env) != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; launch one rank per GPU "
                          "with matching counts")
+    if args.op != "ingest":
+        return run_extract(args)
     return run_ours(args)
 
 

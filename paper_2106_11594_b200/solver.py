@@ -16,7 +16,15 @@ Differences, all deliberate and documented in DESIGN.md:
   * RATIONAL (exact mode) and callable ``alpha`` are CPU-only features of the
     reference and raise CapabilityError here;
   * the stored rank has a device capacity that doubles on demand, so streams
-    behave as if unbounded (the reference reallocates per row, solver.py:112-117).
+    behave as if unbounded (the reference reallocates per row, solver.py:112-117);
+  * ``update`` and ``ingest`` are not bitwise interchangeable.  The reference
+    guarantees that folding ``update`` row by row equals ``ingest`` bit for bit
+    (test_solver.py:212-222).  Here ``update`` runs on the shape-generic kernel
+    (the only one that reports the per-row a-priori residual), while ``ingest``
+    runs on the tensor-core kernels (m 64 / 128 / 256 / up to 1 080 / up to
+    4 736), whose summation orders differ.  The two agree on rank and on every
+    branch outside the rank test's noise band, and x agrees to ~1e-13
+    (tests/test_gpu_parity.py::test_update_fold_matches_ingest).
 """
 
 from __future__ import annotations

@@ -39,12 +39,46 @@ CONFIGS = {
 }
 
 
-def random_standardized(n, m, r, seed):
-    """Restatement of matrices.random_standardized (matrices.py:131-146)."""
+def ordered_product(left, right):
+    """left @ right accumulated over the inner index in a fixed order, each
+    multiply and add rounded separately (no BLAS blocking, no FMA).  The result
+    has the same bits on every CPU and on the GPU (``ordered_product_torch``),
+    which is what lets a golden fixture store only a hash of its inputs: the
+    GPU box regenerates them exactly instead of shipping 100+ MB of rows."""
+    left = np.asarray(left, dtype=np.float64)
+    right = np.asarray(right, dtype=np.float64)
+    A = np.zeros((left.shape[0], right.shape[1]))
+    for j in range(left.shape[1]):
+        A += np.multiply.outer(left[:, j], right[j])
+    return A
+
+
+def ordered_product_torch(left, right):
+    """``ordered_product`` on a torch device: elementwise multiply, then add,
+    in the same order -- bit-identical to the numpy version."""
+    import torch
+
+    A = torch.zeros((left.shape[0], right.shape[1]), dtype=torch.float64, device=left.device)
+    for j in range(left.shape[1]):
+        A.add_(left[:, j, None] * right[None, j, :])
+    return A
+
+
+def random_standardized(n, m, r, seed, ordered=False):
+    """Restatement of matrices.random_standardized (matrices.py:131-146).
+    ``ordered`` forms the product with ``ordered_product`` instead of BLAS
+    (same factors, CPU-independent bits; used by the full-length goldens)."""
     rng = np.random.default_rng(seed)
     left = rng.standard_normal((n, r))
     right = rng.standard_normal((r, m))
-    return left @ right
+    return ordered_product(left, right) if ordered else left @ right
+
+
+def random_standardized_factors(n, m, r, seed):
+    """The factors (left n x r, right r x m) that random_standardized multiplies."""
+    rng = np.random.default_rng(seed)
+    left = rng.standard_normal((n, r))
+    return left, rng.standard_normal((r, m))
 
 
 def c1():
@@ -56,26 +90,26 @@ def c1():
     return A, y
 
 
-def c2():
-    A = random_standardized(4096, 1024, 64, 0)
+def c2(ordered=False):
+    A = random_standardized(4096, 1024, 64, 0, ordered)
     return A, np.random.default_rng(1).standard_normal(4096)
 
 
-def c4():
-    A = random_standardized(8192, 2048, 512, 0)
+def c4(ordered=False):
+    A = random_standardized(8192, 2048, 512, 0, ordered)
     return A, np.random.default_rng(1).standard_normal(8192)
 
 
-def c3_stream(b, n=512, m=128):
+def c3_stream(b, n=512, m=128, ordered=False):
     """Stream b of config 3: r_b ~ U{4..32}; seeds keyed by (3, b, .)."""
     r = int(np.random.default_rng(np.random.SeedSequence([3, b, 0])).integers(4, 33))
     seed = int(np.random.SeedSequence([3, b, 1]).generate_state(1, np.uint64)[0])
-    A = random_standardized(n, m, r, seed)
+    A = random_standardized(n, m, r, seed, ordered)
     y = np.random.default_rng(np.random.SeedSequence([3, b, 2])).standard_normal(n)
     return A, y, r
 
 
-def c5_stream(b, n=1024, m=64, r=16, k=8):
+def c5_stream(b, n=1024, m=64, r=16, k=8, ordered=False):
     """Stream b of config 5: even b Gaussian factors, odd b integer factors
     uniform in {-3..3} (exact rank detection); k N(0,1) right-hand sides."""
     rng = np.random.default_rng(np.random.SeedSequence([5, b]))
@@ -86,24 +120,34 @@ def c5_stream(b, n=1024, m=64, r=16, k=8):
         g1 = rng.integers(-3, 4, (n, r)).astype(np.float64)
         g2 = rng.integers(-3, 4, (r, m)).astype(np.float64)
     Y = rng.standard_normal((n, k))
-    return g1 @ g2, Y
+    return (ordered_product(g1, g2) if ordered else g1 @ g2), Y
 
 
-def host_batch(cfg_name, streams, n=None):
+def host_batch(cfg_name, streams, n=None, ordered=False):
     """rows[S, n, m], targets[S, n, k] for the listed global stream indices."""
     cfg = CONFIGS[cfg_name]
     n = n or cfg.n
     rows, tg = [], []
     for b in streams:
         if cfg_name == "c5":
-            A, Y = c5_stream(b, cfg.n, cfg.m, cfg.r, cfg.k)
+            A, Y = c5_stream(b, cfg.n, cfg.m, cfg.r, cfg.k, ordered)
         elif cfg_name == "c3":
-            A, y, _ = c3_stream(b, cfg.n, cfg.m)
+            A, y, _ = c3_stream(b, cfg.n, cfg.m, ordered)
             Y = y[:, None]
         else:
             raise ValueError("host_batch covers the batched configs c3 and c5")
         rows.append(A[:n]); tg.append(Y[:n])
     return np.stack(rows), np.stack(tg)
+
+
+def input_digest(*arrays):
+    """sha256 over the float64 bytes of the given arrays (golden input pins)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
 
 
 def device_batch(cfg_name, b0, b1, device, dtype=None, chunk=2048):

@@ -142,9 +142,98 @@ def bench_cells():
     np.savez_compressed(os.path.join(OUT, "bench_cells.npz"), **out)
 
 
+# -- full-length fixtures (outputs only; inputs regenerated from the seeds) ------
+
+def ref_trace(A, Y):
+    """The reference's ingest fast path (solver.py:252-319) one row at a time on
+    one RecursiveSolver: branch per row (rank change), the rank-test margin
+    rho = |rej| / (eps max(1, |a|)) from the reference's own `project`
+    (solver.py:210-219) at the current rank, and x for every right-hand side
+    from `solve_batch` (one call per RHS; the reference has no multi-RHS API).
+    The one-row ingests must reproduce solve_batch's x bit for bit."""
+    Y = np.asarray(Y, dtype=np.float64).reshape(A.shape[0], -1)
+    n, m = A.shape
+    s = solver.RecursiveSolver(m)
+    eps_m = np.finfo(np.float64).eps
+    branch = np.zeros(n, np.uint8)
+    rho = np.zeros(n, np.float64)
+    for i in range(n):
+        r0 = s.rank
+        p = s.project(A[i])
+        eps = (m * m * r0 + m * r0 + m) * eps_m
+        rho[i] = np.sqrt(float(p.rejection_sq_norm) / (eps * eps * max(1.0, float(np.dot(A[i], A[i])))))
+        s.ingest(A[i:i + 1], Y[i:i + 1, 0])
+        branch[i] = s.rank > r0
+    xs = []
+    rank = None
+    for c in range(Y.shape[1]):
+        x, rank = solver.solve_batch(A, Y[:, c])
+        xs.append(x)
+    assert rank == s.rank and np.array_equal(xs[0], s.solution), "one-row ingests != solve_batch"
+    return branch, rho.astype(np.float32), rank, np.stack(xs, axis=1)
+
+
+def _c5_trace(b):
+    A, Y = workloads.c5_stream(b, ordered=True)
+    return (b,) + ref_trace(A, Y) + (workloads.input_digest(A, Y),)
+
+
+def _c3_trace(b):
+    A, y, r = workloads.c3_stream(b, ordered=True)
+    return (b,) + ref_trace(A, y) + (workloads.input_digest(A, y),)
+
+
+def runaway_scan(count):
+    """Host-seeded config-5 streams [0, count) whose C-oracle run leaves the
+    construction rank (SURVEY.md finding 0.3): candidates for the golden's
+    runaway streams (the reference itself decides which really run away)."""
+    sys.path.insert(0, os.path.join(OUT, "..", ".."))
+    from oracle import oracle
+
+    found = []
+    for c0 in range(0, count, 1024):
+        rows, tg = workloads.host_batch("c5", range(c0, c0 + 1024), ordered=True)
+        o = oracle.ingest(rows, tg, r_cap=17, nthreads=os.cpu_count() or 8, logs=False)
+        found += [c0 + int(i) for i in np.nonzero(o["status"] & 1)[0]]
+    return found
+
+
+def full_length():
+    """Reference-run full-length fixtures for every config:
+    C2 (4 096 rows), C4 (8 192 rows), 64 C5 streams with all 8 RHS plus streams
+    on which the reference runs away, 64 C3 streams."""
+    from multiprocessing import Pool
+
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    for name, fn in (("c2", workloads.c2), ("c4", workloads.c4)):
+        A, y = fn(ordered=True)
+        branch, rho, rank, X = ref_trace(A, y)
+        np.savez_compressed(os.path.join(OUT, f"full_{name}.npz"), digest=workloads.input_digest(A, y),
+                            branch=branch, rho=rho, rank=rank, x=X[:, 0])
+        print(name, "rank", rank, "max dependent rho", float(rho[branch == 0].max()))
+    runaway = runaway_scan(8192)
+    print("oracle runaway candidates", runaway)
+    streams = list(range(60)) + runaway[:8]
+    with Pool(os.cpu_count() or 8) as p:
+        res = p.map(_c5_trace, streams, chunksize=1)
+    np.savez_compressed(os.path.join(OUT, "full_c5.npz"), streams=np.array([t[0] for t in res]),
+                        branch=np.stack([t[1] for t in res]), rho=np.stack([t[2] for t in res]),
+                        rank=np.array([t[3] for t in res]), x=np.stack([t[4] for t in res]),
+                        digest=np.array([t[5] for t in res]))
+    print("c5 ranks", [t[3] for t in res])
+    with Pool(os.cpu_count() or 8) as p:
+        res = p.map(_c3_trace, list(range(64)), chunksize=1)
+    np.savez_compressed(os.path.join(OUT, "full_c3.npz"), streams=np.array([t[0] for t in res]),
+                        branch=np.stack([t[1] for t in res]), rho=np.stack([t[2] for t in res]),
+                        rank=np.array([t[3] for t in res]), x=np.stack([t[4] for t in res]),
+                        digest=np.array([t[5] for t in res]))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["bench"]:
         bench_cells()
+    elif sys.argv[1:] == ["full"]:
+        full_length()
     else:
         main()
         bench_cells()

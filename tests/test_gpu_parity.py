@@ -2,9 +2,11 @@
 
 Bar (BASELINE.json north star): identical detected ranks and branch
 sequences; x and A+ within 1e-9 relative (fp64), 1e-3 (fp32), with the error
-metric of test_acceptance.py:56-61.  Rows whose oracle rank-test margin
-rho = |rej| / (eps max(1, |a|)) lies in [1/4, 4] are "ambiguous": they are
-counted and reported, and strict branch equality is asserted on the others.
+metric of test_acceptance.py:56-61.  A stream's first branch disagreement
+with the oracle is tolerated only on a row whose rank-test margin
+rho = |rej| / (eps max(1, |a|)) lies in the noise band (rgb_testutil.BAND,
+[1/16, 16], measured between the reference and the oracle); it is counted,
+and everything before it must match row for row.
 """
 
 import numpy as np
@@ -214,27 +216,38 @@ def test_rank_capacity_grows_like_the_reference():
 
 # -- full-size configurations against the C oracle --------------------------------
 
-def ambiguous_rows(rho):
-    """Rows whose oracle rank-test margin is within a factor 8 of the threshold:
-    a dependent row's rejection is pure rounding noise, whose size depends on
-    the summation order, so two correct fp64 implementations can land on
-    opposite sides of the threshold there (hard part 1)."""
-    return (rho >= 0.125) & (rho <= 8.0)
-
-
 def compare_to_oracle(rows, targets, res, r_cap, tol=TOL64, variant="general", alpha=1.0, out=None):
+    """Device run against the C oracle on the same bytes: the first branch
+    disagreement of a stream (if any) must sit on a row whose oracle margin is
+    in the noise band (rgb_testutil.BAND); ranks and x must match on every
+    stream whose branch log matches.  Returns (streams not exactly matched,
+    worst x error)."""
+    from rgb_testutil import compare_branches
+
     o = oracle.ingest(rows, targets, r_cap=r_cap, variant=variant, alpha=alpha, nthreads=8)
     if out is not None:
         out.update(o)
-    amb_rows = ambiguous_rows(o["rho"])
-    amb = amb_rows.any(axis=1) | (o["status"] != 0) | (res["status"] != 0)
-    ok = ~amb
+    cmp = compare_branches(res["branch"], res["nobs"], o["branch"], o["rho"])
+    assert cmp["outside_disagree"] == 0, cmp["disagreements"]
+    ok = np.array([res["status"][b] == 0 and o["status"][b] == 0 and np.array_equal(res["branch"][b], o["branch"][b])
+                   for b in range(rows.shape[0])])
     assert np.array_equal(res["rank"][ok], o["rank"][ok])
-    assert np.array_equal(res["branch"][ok], o["branch"][ok])
     X = oracle.solution(o)
     worst = max((relerr(res["x"][b], X[b]) for b in np.nonzero(ok)[0]), default=0.0)
     assert worst <= tol, worst
-    return int(amb.sum()), worst
+    return int((~ok).sum()), worst
+
+
+def matched(branch, nobs, status, o):
+    """Mask of streams whose device branch log equals the oracle's row for row
+    (neither frozen); asserts that every other stream's first disagreement is
+    on a noise-band row (rgb_testutil.compare_branches)."""
+    from rgb_testutil import compare_branches
+
+    cmp = compare_branches(branch, nobs, o["branch"], o["rho"])
+    assert cmp["outside_disagree"] == 0, cmp["disagreements"]
+    return np.array([status[b] == 0 and o["status"][b] == 0 and np.array_equal(branch[b], o["branch"][b])
+                     for b in range(len(status))])
 
 
 def test_c5_full_length_streams_against_oracle():
@@ -382,17 +395,15 @@ def test_c5_parity_at_scale_device_generated():
     torch.cuda.synchronize()
     rows, tg = rows_d.cpu().numpy(), tg_d.cpu().numpy()
     o = oracle.ingest(rows, tg, r_cap=16, nthreads=16)
-    amb = ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0)
-    ok = ~amb
-    st = bs.status.cpu().numpy()
-    assert (st[ok] == 0).all()
+    ok = matched(br.cpu().numpy(), bs.nobs_t.cpu().numpy(), bs.status.cpu().numpy(), o)
     assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
-    assert np.array_equal(br.cpu().numpy()[ok], o["branch"][ok])
     X = bs.solution.cpu().numpy()
     XO = oracle.solution(o)
     worst = max(relerr(X[b], XO[b]) for b in np.nonzero(ok)[0])
-    assert worst <= 1e-10
-    assert amb.mean() < 0.02, amb.mean()
+    # streams with near-threshold rows are ill conditioned: x differs up to
+    # ~1e-9 there (median 6e-16); the north-star bar is 1e-9
+    assert worst <= TOL64
+    assert (~ok).mean() < 0.02, (~ok).mean()
 
 
 @pytest.mark.parametrize("cfg,r_cap,splits", [("c5", 16, (40, 300, 1024)), ("c3", 32, (13, 200, 512))])
@@ -406,7 +417,7 @@ def test_continuation_calls_match_one_shot(cfg, r_cap, splits):
     rows, tg = workloads.host_batch(cfg, list(range(24)))
     B, n, m = rows.shape
     k = tg.shape[2]
-    one = run_batched(rows, tg, r_cap=r_cap, logs=False)
+    one = run_batched(rows, tg, r_cap=r_cap)
     bs = BatchedSolver(B, m, k=k, r_cap=r_cap)
     lo = 0
     for hi in splits:
@@ -414,8 +425,7 @@ def test_continuation_calls_match_one_shot(cfg, r_cap, splits):
         lo = hi
     torch.cuda.synchronize()
     o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=8)
-    amb = ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0)
-    ok = ~amb
+    ok = matched(one["branch"], one["nobs"], one["status"], o)
     X = bs.solution.cpu().numpy()
     assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
     assert (bs.nobs_t.cpu().numpy()[ok] == n).all()
@@ -434,10 +444,9 @@ def test_fixed_eps_policy_on_blocked_kernels(cfg, r_cap):
     for eps in (1e-8, 1e-3):
         res = run_batched(rows, tg, r_cap=r_cap, eps=eps)
         o = oracle.ingest(rows, tg, r_cap=r_cap, eps=eps)
-        amb = ((o["rho"] >= 0.125) & (o["rho"] <= 8.0)).any(axis=1)
-        ok = ~amb
+        ok = matched(res["branch"], res["nobs"], res["status"], o)
         assert np.array_equal(res["rank"][ok], o["rank"][ok])
-        assert np.array_equal(res["branch"][ok], o["branch"][ok])
+        assert ok.sum() >= len(ok) - 1
 
 
 def test_c3_parity_at_scale_device_generated():
@@ -452,15 +461,13 @@ def test_c3_parity_at_scale_device_generated():
     torch.cuda.synchronize()
     rows, tg = rows_d.cpu().numpy(), tg_d.cpu().numpy()
     o = oracle.ingest(rows, tg, r_cap=32, nthreads=16)
-    amb = ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0)
-    ok = ~amb
+    ok = matched(br.cpu().numpy(), bs.nobs_t.cpu().numpy(), bs.status.cpu().numpy(), o)
     assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
-    assert np.array_equal(br.cpu().numpy()[ok], o["branch"][ok])
     X = bs.solution.cpu().numpy()
     XO = oracle.solution(o)
     worst = max(relerr(X[b], XO[b]) for b in np.nonzero(ok)[0])
     assert worst <= 1e-9
-    assert amb.mean() < 0.02
+    assert (~ok).mean() < 0.02
 
 
 @pytest.mark.parametrize("cfg,r_cap", [("c5", 16), ("c3", 32)])
@@ -474,7 +481,7 @@ def test_tensor_core_kernel_agrees_with_generic_kernel(cfg, r_cap):
     blk = run_batched(rows, tg, r_cap=r_cap)
     gen = run_batched(rows, tg, r_cap=r_cap, resid=True)
     o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=8)
-    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0))
+    ok = matched(blk["branch"], blk["nobs"], blk["status"], o) & matched(gen["branch"], gen["nobs"], gen["status"], o)
     assert np.array_equal(blk["branch"][ok], gen["branch"][ok])
     assert np.array_equal(blk["rank"][ok], gen["rank"][ok])
     for b in np.nonzero(ok)[0]:
@@ -624,7 +631,7 @@ def test_variants_on_tensor_core_kernel(cfg, r_cap, n, variant, alpha):
     o = {}
     amb, worst = compare_to_oracle(rows, tg, res, r_cap=r_cap, variant=variant, alpha=alpha, out=o)
     assert amb <= 2 and worst <= 1e-10, (amb, worst)
-    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (res["status"] != 0))
+    ok = matched(res["branch"], res["nobs"], res["status"], o)
     bs = res["solver"]
     C, D, P = (t.cpu().numpy() for t in (bs.basis_t, bs.dual_t, bs.gram_t))
     for b in np.nonzero(ok)[0]:
@@ -865,7 +872,6 @@ def test_one_warp_kernel_fewer_right_hand_sides(k):
     rows, tg = workloads.host_batch("c5", list(range(40)), n=300)
     tg = np.ascontiguousarray(tg[..., :k])
     o = oracle.ingest(rows, tg, r_cap=16, nthreads=8)
-    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0))
     for split in (None, 133):
         bs = BatchedSolver(40, 64, k=k, r_cap=16)
         br = torch.zeros((40, 300), dtype=torch.uint8, device="cuda")
@@ -878,7 +884,8 @@ def test_one_warp_kernel_fewer_right_hand_sides(k):
             bs.ingest(dev(rows[:, split:]), dev(tg[:, split:]), branch_log=b2)
             br = torch.cat([b1, b2], dim=1)
         torch.cuda.synchronize()
-        assert np.array_equal(br.cpu().numpy()[ok], o["branch"][ok])
+        ok = matched(br.cpu().numpy(), bs.nobs_t.cpu().numpy(), bs.status.cpu().numpy(), o)
+        assert ok.sum() >= 38
         assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok])
         X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
         assert X.shape == (40, 64, k)
@@ -942,7 +949,7 @@ def test_batched_covariance_matches_closed_form(cfg, r_cap, variant):
     rows, tg = workloads.host_batch(cfg, list(range(12)), n=200)
     res = run_batched(rows, tg, r_cap=r_cap, variant=variant)
     o = oracle.ingest(rows, tg, r_cap=r_cap, variant=variant, nthreads=8)
-    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0))
+    ok = matched(res["branch"], res["nobs"], res["status"], o)
     bs = res["solver"]
     V = bs.covariance().cpu().numpy()
     pinv = bs.pinv(dev(res["coords"])).cpu().numpy()
@@ -985,10 +992,6 @@ def test_random_shapes_against_oracle(seed):
         rows, tg = _lowrank_streams(B, n, m, r, k, seed=int(rng.integers(1 << 30)))
         alpha = float(rng.uniform(0.5, 2.0)) if variant == "orthogonal" else 1.0
         o = oracle.ingest(rows, tg, r_cap=r_cap, variant=variant, alpha=alpha, nthreads=8)
-        # excluded like everywhere else: ambiguous rows, and runaways -- the
-        # reference itself can read rounding noise as rank (oracle rank above the
-        # construction rank), after which x is noise-dominated in any implementation
-        ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (o["rank"] != r))
         bs = BatchedSolver(B, m, k=k, r_cap=r_cap, variant=variant, alpha=alpha)
         split = int(rng.integers(0, n))
         b1 = torch.zeros((B, split), dtype=torch.uint8, device="cuda")
@@ -999,7 +1002,10 @@ def test_random_shapes_against_oracle(seed):
         torch.cuda.synchronize()
         br = torch.cat([b1, b2], dim=1).cpu().numpy()
         case = (m, r_cap, k, variant, B, r, n, split)
-        assert np.array_equal(br[ok], o["branch"][ok]), case
+        # a first branch disagreement only on a noise-band row; runaways (the
+        # oracle reading rounding noise as rank past the construction rank,
+        # after which x is noise-dominated in any implementation) not compared
+        ok = matched(br, bs.nobs_t.cpu().numpy(), bs.status.cpu().numpy(), o) & (o["rank"] == r)
         assert np.array_equal(bs.rank.cpu().numpy()[ok], o["rank"][ok]), case
         X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
         for b in np.nonzero(ok)[0]:
@@ -1026,10 +1032,9 @@ def test_warp_group_kernel_other_instantiations(m, r_cap, variant, no_panel, mon
     rows = np.stack([_lowrank_streams(1, n, m, int(r), 1, seed=int(b))[0][0] for b, r in enumerate(rs)])
     tg = rng.standard_normal((B, n, 1))
     o = oracle.ingest(rows, tg, r_cap=r_cap, variant=variant, nthreads=8)
-    ok = ~(ambiguous_rows(o["rho"]).any(axis=1) | (o["status"] != 0) | (o["rank"] != rs))
-    assert ok.sum() >= B - 2
     res = run_batched(rows, tg, r_cap=r_cap, variant=variant)
-    assert np.array_equal(res["branch"][ok], o["branch"][ok])
+    ok = matched(res["branch"], res["nobs"], res["status"], o) & (o["rank"] == rs)
+    assert ok.sum() >= B - 2
     assert np.array_equal(res["rank"][ok], o["rank"][ok])
     X = oracle.solution(o)
     assert max(relerr(res["x"][b], X[b]) for b in np.nonzero(ok)[0]) <= 1e-10
@@ -1110,3 +1115,141 @@ def test_bench_two_ranks_equal_one_rank(tmp_path):
         assert np.array_equal(a[key], b[key]), key
     # value counts the rows actually folded (sum of nobs)
     assert abs(line["value"] * line["ms_per_step"] * 1e-3 - int(a["nobs"].sum())) <= 1e-6 * a["nobs"].sum()
+
+
+# -- interleaved dependent rows before the rank is reached --------------
+
+def _interleaved_stream(n, m, r, seed):
+    """Rows where dependent rows (exact duplicates and in-span combinations of
+    rows already seen) are interleaved with the r independent rows, so tiles
+    hold dependent rows followed by an independent one before the rank is
+    reached -- the case the generic low-rank recipes (first r rows independent)
+    never produce."""
+    rng = np.random.default_rng(seed)
+    basis = rng.standard_normal((r, m))
+    rows, seen, nxt = [], [], 0
+    while len(rows) < n:
+        new = nxt < r and (not seen or rng.random() < 0.4)
+        if new:
+            rows.append(basis[nxt])
+            seen.append(nxt)
+            nxt += 1
+        elif rng.random() < 0.3:
+            rows.append(basis[seen[int(rng.integers(len(seen)))]].copy())  # exact duplicate
+        else:
+            c = rng.standard_normal(len(seen))
+            rows.append(c @ basis[seen])  # in-span combination
+    return np.ascontiguousarray(np.array(rows)), rng.standard_normal((n, 1)), nxt
+
+
+@pytest.mark.parametrize("m,r_cap,r,n", [(2048, 64, 50, 200), (2048, 512, 120, 300), (1024, 64, 60, 240)])
+@pytest.mark.parametrize("variant,alpha", [("general", 1.0), ("orthogonal", 0.7), ("orthonormal", 1.0)])
+def test_large_stream_kernels_interleaved_dependent_rows(m, r_cap, r, n, variant, alpha):
+    """The grid kernel (m 2048) and the cluster kernel (m 1024) on streams whose
+    dependent rows precede independent ones inside 8-row tiles: the grid
+    kernel's deferred P fold and its U / S partials formed before the rank
+    test, and the cluster home's panel fold, against the oracle's branches,
+    P, C, C~ and x."""
+    rows, tg, r = _interleaved_stream(n, m, r, seed=m + r_cap + r)  # r: independent rows emitted
+    res = run_batched(rows, tg, r_cap=r_cap, variant=variant, alpha=alpha)
+    o = oracle.ingest(rows[None], tg[None], r_cap=r_cap, variant=variant, alpha=alpha)
+    assert res["status"][0] == 0
+    assert int(res["rank"][0]) == int(o["rank"][0]) == r
+    br = o["branch"][0]
+    # the construction really interleaves: some dependent row precedes an independent one in a tile
+    first_dep = np.nonzero(br == 0)[0][0]
+    assert first_dep < np.nonzero(br == 1)[0][-1]
+    assert np.array_equal(res["branch"][0], br)
+    assert relerr(res["x"][0], oracle.solution(o)[0]) <= 1e-10
+    bs = res["solver"]
+    C = bs.basis_t[0, :r].cpu().numpy()
+    D = bs.dual_t[0, :r].cpu().numpy()
+    P = bs.gram_t[0, :r, :r].cpu().numpy()
+    assert relerr(C, o["C"][0, :r]) <= 1e-10
+    assert relerr(D, (o["C"] if variant == "orthonormal" else o["D"])[0, :r]) <= 1e-10
+    assert relerr(P, o["P"][0, :r, :r]) <= 1e-8
+    assert relerr(res["coords"][0], o["coords"][0]) <= 1e-9
+
+
+# -- update() fold against ingest() (ADVICE r1) ---------------------------------------
+
+@pytest.mark.parametrize("m,n", [(128, 300), (1024, 160)])
+def test_update_fold_matches_ingest(m, n):
+    """The drop-in update() runs every call on the generic kernel (it reports
+    per-row residuals), ingest() on the tensor-core kernels.  The reference
+    guarantees the two agree bit for bit (test_solver.py:212-222); here they
+    are different summation orders, so the bar is: identical branches on every
+    row outside the noise band, identical rank, x within 1e-9 -- and the
+    update() branches equal the oracle's."""
+    import paper_2106_11594_b200 as p
+    from paper_2106_11594_b200 import workloads
+    from rgb_testutil import compare_branches
+
+    if m == 128:
+        rows, tg = workloads.host_batch("c3", [7], n=n)
+        A, y = rows[0], tg[0, :, 0]
+    else:
+        A, y = workloads.c2()
+        A, y = A[:n], y[:n]
+    su = p.RecursiveSolver(m)
+    br = np.array([su.update(a, t).branch == "independent" for a, t in zip(A, y)], np.uint8)
+    si = p.RecursiveSolver(m)
+    si.ingest(A, y)
+    o = oracle.ingest(A[None], y[None], r_cap=m)
+    cmp = compare_branches(br[None], None, o["branch"], o["rho"])
+    assert cmp["outside_disagree"] == 0 and cmp["exact"] == 1
+    assert su.rank == si.rank == int(o["rank"][0])
+    assert relerr(su.solution, si.solution) <= 1e-9
+    assert relerr(si.solution, oracle.solution(o)[0, :, 0]) <= 1e-9
+
+
+# -- A+ / covariance extraction on the fp64 tensor cores ----------------------------
+
+@pytest.mark.parametrize("m,r_cap,n,B", [(64, 16, 40, 3), (37, 8, 29, 2), (130, 32, 70, 2), (1024, 64, 300, 1)])
+def test_pinv_and_covariance_shapes_against_oracle(m, r_cap, n, B):
+    """rgb_pinv / rgb_covariance (two DMMA contractions, V = P^-1 C~ then V^T B^T
+    or V^T C~) on tile-ragged shapes (odd m, n not a multiple of 64, ranks below
+    the capacity): against the oracle's closed form C~^T P^-1 B^T."""
+    rng = np.random.default_rng(m * 7 + n)
+    rs = rng.integers(1, min(r_cap, m) + 1, size=B)
+    rows = np.stack([_lowrank_streams(1, n, m, int(r), 1, seed=int(b) + m)[0][0] for b, r in enumerate(rs)])
+    tg = rng.standard_normal((B, n, 1))
+    res = run_batched(rows, tg, r_cap=r_cap)
+    o = oracle.ingest(rows, tg, r_cap=r_cap, nthreads=8)
+    ok = matched(res["branch"], res["nobs"], res["status"], o)
+    assert ok.all()
+    bs = res["solver"]
+    pinv = bs.pinv(dev(res["coords"])).cpu().numpy()
+    V = bs.covariance().cpu().numpy()
+    for b in range(B):
+        ob = {key: v[b:b + 1] for key, v in o.items() if isinstance(v, np.ndarray)}
+        po = oracle.pinv_closed_form(ob)
+        assert relerr(pinv[b], po) <= 1e-9, b
+        assert relerr(V[b], po @ po.T) <= 1e-9, b
+
+
+def test_pinv_and_covariance_at_the_config5_batch():
+    """65 536 streams (the config-5 batch, past the 65 535 grid.y limit of a
+    single launch): A+ and the covariance of every stream, checked on streams
+    spread over both launch chunks."""
+    from paper_2106_11594_b200.batched import BatchedSolver
+
+    B, n, m = 65536, 24, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    rows = torch.bmm(torch.randn(B, n, 4, generator=g, device="cuda", dtype=torch.float64),
+                     torch.randn(B, 4, m, generator=g, device="cuda", dtype=torch.float64))
+    tg = torch.randn(B, n, 8, generator=g, device="cuda", dtype=torch.float64)
+    bs = BatchedSolver(B, m, k=8, r_cap=16)
+    coords = torch.zeros((B, n, 16), dtype=torch.float64, device="cuda")
+    bs.ingest(rows, tg, coords_log=coords)
+    pinv = bs.pinv(coords)
+    V = bs.covariance()
+    torch.cuda.synchronize()
+    for b in (0, 1, 40000, 65534, 65535):
+        A = rows[b].cpu().numpy()
+        o = oracle.ingest(A[None], tg[b].cpu().numpy()[None], r_cap=16)
+        po = oracle.pinv_closed_form(o)
+        assert int(bs.rank[b]) == int(o["rank"][0]) == 4
+        assert relerr(pinv[b].cpu().numpy(), po) <= 1e-9
+        assert relerr(V[b].cpu().numpy(), po @ po.T) <= 1e-9
+        assert relerr(pinv[b].cpu().numpy(), np.linalg.pinv(A, rcond=1e-10)) <= 1e-8
