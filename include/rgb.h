@@ -3,9 +3,12 @@
  * library (librgb.so).  arXiv 2106.11594, Algorithm 1.
  *
  * Plain C: raw device pointers, sizes and a cudaStream_t passed as void*.
- * The caller owns every buffer (allocate with cudaMalloc, torch, cupy ...);
- * the library allocates nothing and keeps no state between calls except a
- * thread-local error string.  Every call is asynchronous on `stream`.
+ * The caller owns every state and input buffer (allocate with cudaMalloc,
+ * torch, cupy ...); the library keeps no state between calls except a
+ * thread-local error string, stream-ordered scratch from a library-owned
+ * device memory pool (grid kernel, A+ / covariance), and the row pipes the
+ * caller creates and destroys explicitly.  Every call is asynchronous on
+ * `stream` except rgb_rowpipe_run, which returns with the row folded.
  * Calls on one state must be stream-ordered (single writer, as SPEC.md:197);
  * distinct states may run concurrently on different streams or GPUs.
  *
@@ -22,7 +25,7 @@
 extern "C" {
 #endif
 
-#define RGB_ABI_VERSION 2
+#define RGB_ABI_VERSION 3
 
 /* scalar kinds: scalars.py:141-147 (FLOAT64); FLOAT32 is a new kind */
 enum { RGB_F64 = 0, RGB_F32 = 1 };
@@ -146,6 +149,39 @@ int rgb_memcpy_async(void *dst, const void *src, int64_t bytes, void *stream);
 /* Covariance V = A+ A+^T = C~^T P^-1 C~ (CovarianceTracker.covariance,
  * tracking.py:88-119; identity of test_tracking.py:188-198): out [B][m][m]. */
 int rgb_covariance(const rgb_config *cfg, const rgb_state *state, void *out, void *stream);
+
+/* ---- low-latency one-row pipe (the drop-in per-row API) -------------------
+ * RecursiveSolver.update (solver.py:231-250) and a one-row ingest are latency
+ * bound.  A row pipe belongs to ONE stream's state (num_streams == 1) and owns
+ * a pinned, device-mapped host block and a CUDA graph: the shape-generic
+ * kernel reads the row (m values) and targets (k values) from the block's
+ * input area and writes the report into it; the counters follow, then a
+ * sequence word.  rgb_rowpipe_run launches the graph on `stream` and returns
+ * once the report is visible (it spins on the sequence word; no stream
+ * synchronisation).  Recreate the pipe when the state buffers move (capacity
+ * growth).  Block layout (bytes): header of RGB_ROWPIPE_HEADER -- sequence
+ * u64 @0, nobs i64 @8, rank i32 @16, status i32 @20, branch u8 @24 (1 =
+ * independent) -- then the areas whose offsets rgb_rowpipe_layout returns:
+ * input (row then targets, float when f32in or an RGB_F32 state, else
+ * double), a-priori residuals [k] and gain [m] (the state's type). */
+#define RGB_ROWPIPE_HEADER 64
+#define RGB_ROWPIPE_OFF_SEQ 0
+#define RGB_ROWPIPE_OFF_NOBS 8
+#define RGB_ROWPIPE_OFF_RANK 16
+#define RGB_ROWPIPE_OFF_STATUS 20
+#define RGB_ROWPIPE_OFF_BRANCH 24
+typedef struct rgb_rowpipe rgb_rowpipe;
+
+/* Size of a row pipe's host block (bytes) and the offsets of its areas. */
+int64_t rgb_rowpipe_layout(const rgb_config *cfg, int f32in, int64_t *off_in, int64_t *off_resid,
+                           int64_t *off_gain);
+/* Capture the pipe for `state` (report logs when want_report); *host_block
+ * receives the block the caller fills and reads. */
+int rgb_rowpipe_create(const rgb_config *cfg, const rgb_state *state, int want_report, int f32in,
+                       rgb_rowpipe **pipe, void **host_block);
+/* Fold the row staged in the block; blocks until its report is visible. */
+int rgb_rowpipe_run(rgb_rowpipe *pipe, void *stream);
+void rgb_rowpipe_destroy(rgb_rowpipe *pipe);
 
 #ifdef __cplusplus
 }

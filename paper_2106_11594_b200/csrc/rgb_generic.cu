@@ -20,6 +20,29 @@
 namespace rgb {
 
 constexpr int GEN_NT = 256;
+
+// phase timing (debug builds only: -DRGB_GEN_PROBE): %globaltimer ns summed per
+// phase by thread 0 of CTA 0, read back with rgb_generic_probe()
+#ifdef RGB_GEN_PROBE
+__device__ unsigned long long g_genprobe[16];
+__device__ __forceinline__ unsigned long long gen_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GENPROBE(i)                                             \
+  do {                                                          \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                  \
+      const unsigned long long now_ = gen_now();                \
+      g_genprobe[i] += now_ - probe_t;                          \
+      probe_t = now_;                                           \
+    }                                                           \
+  } while (0)
+#else
+#define GENPROBE(i) \
+  do {              \
+  } while (0)
+#endif
 constexpr int GEN_NW = GEN_NT / 32;
 constexpr int GEN_MAX_K = 64;
 
@@ -42,11 +65,51 @@ __device__ __forceinline__ void block_reduce(int nv, REAL* red, REAL* out, F par
   __syncthreads();
 }
 
+__device__ __forceinline__ void cp_async_n(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+  else if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Asynchronous global -> shared copy of n contiguous elements (16-byte pieces
+// when both ends are 16-byte aligned); the caller commits and waits.
+template <typename REAL>
+__device__ __forceinline__ void stage_async(REAL* dst, const REAL* src, int64_t n, int tid) {
+  constexpr int V = 16 / sizeof(REAL);
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const int64_t nv = n / V;
+    for (int64_t e = tid; e < nv; e += GEN_NT) cp_async_n(dst + e * V, src + e * V, 16);
+    for (int64_t e = nv * V + tid; e < n; e += GEN_NT) cp_async_n(dst + e, src + e, sizeof(REAL));
+  } else {
+    for (int64_t e = tid; e < n; e += GEN_NT) cp_async_n(dst + e, src + e, sizeof(REAL));
+  }
+}
+
+// Row pipe (rgb_rowpipe.cu): the counters, then the sequence word, into the
+// caller's mapped host block; a barrier plus one system-scope release order
+// every thread's report writes before the sequence word the host spins on.
+__device__ __forceinline__ void publish_row_report(unsigned char* mirror, unsigned long long* dseq, int64_t nobs,
+                                                   int r, int status, int tid) {
+  __syncthreads();  // every thread's report writes happen before thread 0's release below
+  if (tid == 0) {
+    *reinterpret_cast<volatile int64_t*>(mirror + RGB_ROWPIPE_OFF_NOBS) = nobs;
+    *reinterpret_cast<volatile int32_t*>(mirror + RGB_ROWPIPE_OFF_RANK) = r;
+    *reinterpret_cast<volatile int32_t*>(mirror + RGB_ROWPIPE_OFF_STATUS) = status;
+    const unsigned long long sq = *dseq + 1;
+    *dseq = sq;
+    // one system-scope release (cumulative over the barrier): the report and
+    // the counters are visible to the host before the sequence word
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(mirror + RGB_ROWPIPE_OFF_SEQ), "l"(sq) : "memory");
+  }
+}
+
 // TI: input element type (REAL, or float widened exactly into a double state)
 template <typename REAL, typename TI>
 __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rows_stride,
-    const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs, int cached) {
+    const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs, int cached,
+    unsigned char* __restrict__ mirror, unsigned long long* __restrict__ dseq) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
   REAL* a_s = reinterpret_cast<REAL*>(smem_raw);        // m
@@ -60,6 +123,10 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
   REAL* scal = red + GEN_NW * (GEN_MAX_K + 2);           // denom etc.
   REAL* cache = scal + 8;  // cached: the stream's C, C~, P^-1, x (generic_cache_elems)
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#ifdef RGB_GEN_PROBE
+  unsigned long long probe_t = gen_now();
+  if (tid == 0 && blockIdx.x == 0) g_genprobe[15] += 1;
+#endif
 
   for (int64_t b = blockIdx.x; b < cfg.num_streams; b += gridDim.x) {
     REAL* Cg = reinterpret_cast<REAL*>(st.basis) + b * (int64_t)rc * m;
@@ -71,7 +138,10 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
     int r = st.rank[b];
     int status = st.status[b];
     int64_t nobs = st.nobs[b];
-    if (status) continue;
+    if (status) {  // frozen: nothing to fold (a row pipe still publishes its counters)
+      if (mirror) publish_row_report(mirror, dseq, nobs, r, status, tid);
+      continue;
+    }
     const int r0 = r;
     REAL *C = Cg, *D = Dg, *P = Pg, *X = Xg;
     if (cached) {
@@ -82,22 +152,36 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
       D = (var == RGB_ORTHONORMAL) ? C : C + (size_t)rc * m;
       P = C + (size_t)(var == RGB_ORTHONORMAL ? 1 : 2) * rc * m;
       X = P + (size_t)rc * rc;
-#pragma unroll 4
-      for (int e = tid; e < r0 * m; e += GEN_NT) C[e] = Cg[e];
-      if (var != RGB_ORTHONORMAL) {
-#pragma unroll 4
-        for (int e = tid; e < r0 * m; e += GEN_NT) D[e] = Dg[e];
+      // every copy in flight at once (cp.async), one wait: a single L2 round
+      // trip instead of one per unrolled batch of loads
+      stage_async(C, Cg, (int64_t)r0 * m, tid);
+      if (var != RGB_ORTHONORMAL) stage_async(D, Dg, (int64_t)r0 * m, tid);
+      for (int e = tid; e < r0 * r0; e += GEN_NT) {
+        const int i = e / r0, l = e - i * r0;
+        cp_async_n(P + (size_t)i * rc + l, Pg + (size_t)i * rc + l, sizeof(REAL));
       }
-#pragma unroll 4
-      for (int e = tid; e < r0 * r0; e += GEN_NT) P[(e / r0) * rc + e % r0] = Pg[(e / r0) * rc + e % r0];
-#pragma unroll 4
-      for (int e = tid; e < k * m; e += GEN_NT) X[e] = Xg[e];
-    }
-    for (int64_t t = 0; t < T; ++t) {
-      const TI* a = R + t * m;
-      for (int j = tid; j < m; j += GEN_NT) a_s[j] = (REAL)a[j];
-      for (int c = tid; c < k; c += GEN_NT) y_s[c] = (REAL)Y[t * k + c];
+      stage_async(X, Xg, (int64_t)k * m, tid);
+      if constexpr (sizeof(TI) == sizeof(REAL)) {
+        // the first row rides with the state: its latency (an L2 or, for a row
+        // pipe, a host-memory round trip) overlaps the state's
+        if (T > 0) {
+          for (int j = tid; j < m; j += GEN_NT) cp_async_n(a_s + j, R + j, sizeof(REAL));
+          for (int c = tid; c < k; c += GEN_NT) cp_async_n(y_s + c, Y + c, sizeof(REAL));
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
       __syncthreads();
+    }
+    GENPROBE(0);
+    for (int64_t t = 0; t < T; ++t) {
+      if (!(cached && t == 0 && sizeof(TI) == sizeof(REAL))) {
+        const TI* a = R + t * m;
+        for (int j = tid; j < m; j += GEN_NT) a_s[j] = (REAL)a[j];
+        for (int c = tid; c < k; c += GEN_NT) y_s[c] = (REAL)Y[t * k + c];
+        __syncthreads();
+      }
+      GENPROBE(1);
       // coords = C~ a (solver.py:286): warp per dual row, lanes over columns
       for (int i = w; i < r; i += GEN_NW) {
         const REAL* d = D + (int64_t)i * m;
@@ -107,6 +191,7 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
         if (lane == 0) gam[i] = s;
       }
       __syncthreads();
+      GENPROBE(2);
       // rej = a - C^T coords (solver.py:287-288), kept for the independent branch
       for (int j = tid; j < m; j += GEN_NT) {
         REAL s = 0;
@@ -127,6 +212,7 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
         }
         return s;
       });
+      GENPROBE(3);
       const REAL rej_sq = sums[0], row_sq = sums[1];
       bool bad = !isfinite(row_sq);
       for (int c = 0; c < k; ++c) bad |= !isfinite(y_s[c]);
@@ -157,6 +243,7 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
         }
         __syncthreads();
       }
+      GENPROBE(4);
       // rescaling of the stored rejection (orthogonal / orthonormal, solver.py:354-366, 383)
       REAL alpha = 1, last = 1;
       if (!dep && var != RGB_GENERAL) {
@@ -226,6 +313,7 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
       }
       nobs += 1;
       __syncthreads();
+      GENPROBE(5);
     }
     __syncthreads();
     if (cached) {  // write back what the rows changed (rows >= r0 are new; C~ and P^-1 change in place)
@@ -242,8 +330,24 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
       st.nobs[b] = nobs;
       st.status[b] = status;
     }
+    GENPROBE(6);
+    if (mirror) publish_row_report(mirror, dseq, nobs, r, status, tid);
+    GENPROBE(7);
   }
 }
+
+#ifdef RGB_GEN_PROBE
+}  // namespace rgb
+extern "C" int rgb_generic_probe(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rgb::g_genprobe, sizeof(rgb::g_genprobe));
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(rgb::g_genprobe, z, sizeof(z));
+  }
+  return 0;
+}
+namespace rgb {
+#endif
 
 size_t generic_smem_bytes(const rgb_config& cfg) {
   size_t s = cfg.dtype == RGB_F32 ? 4 : 8;
@@ -264,7 +368,8 @@ static constexpr size_t GEN_CACHE_MAX = 96 * 1024;
 
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
-                   cudaStream_t stream, int num_sms, bool f32in) {
+                   cudaStream_t stream, int num_sms, bool f32in, unsigned char* mirror,
+                   unsigned long long* dseq) {
   if (cfg.k > GEN_MAX_K) return RGB_E_UNSUPPORTED;
   size_t smem = generic_smem_bytes(cfg);
   if (smem > 200 * 1024) return RGB_E_UNSUPPORTED;
@@ -277,17 +382,17 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
     auto kern = generic_ingest_kernel<double, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                   (const float*)targets, tg_stride, T, logs, cached);
+                                                   (const float*)targets, tg_stride, T, logs, cached, mirror, dseq);
   } else if (cfg.dtype == RGB_F64) {
     auto kern = generic_ingest_kernel<double, double>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                   (const double*)targets, tg_stride, T, logs, cached);
+                                                   (const double*)targets, tg_stride, T, logs, cached, mirror, dseq);
   } else {
     auto kern = generic_ingest_kernel<float, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                  (const float*)targets, tg_stride, T, logs, cached);
+                                                  (const float*)targets, tg_stride, T, logs, cached, mirror, dseq);
   }
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }

@@ -142,7 +142,8 @@ class RecursiveSolver:
         self._torch = torch
         self._f32in = False
         self._host = {"rank": 0, "nobs": 0}
-        self._graphs = {}  # one-row call graphs (None: capture unsupported)
+        self._pipes = {}  # one-row pipes (librgb rgb_rowpipe), by layout; None: unsupported
+        self._fast = {}   # want_report -> the current pipe's handles, unpacked for update() / ingest()
 
     # -- read-only access ---------------------------------------------------
     @property
@@ -228,6 +229,29 @@ class RecursiveSolver:
         """Ingest one observation; returns an UpdateReport (solver.py:231-250)."""
         row = self._kind.vector(row, self._m)
         target = self._kind.coerce(target)
+        fast = self._fast.get(True) if self._fast else None
+        if fast is not None and fast[0] == self._st_key:
+            # the steady-state per-row path: stage, one row-pipe run, read the report
+            _, pin, run, h, s, hdr_n, hdr_c, hdr_b, resid, gain = fast
+            m = self._m
+            pin[:m] = row
+            pin[m] = target
+            rc = run(h, s)
+            if rc:
+                _lib.check(rc, "rgb_rowpipe_run")
+            nobs = int(hdr_n[0])
+            host = self._host
+            if nobs != host["nobs"] and not hdr_c[1]:
+                host["nobs"] = nobs
+                rank = host["rank"] = int(hdr_c[0])
+                return UpdateReport("independent" if hdr_b[0] else "dependent", gain.copy(), float(resid[0]), rank)
+            # a stop (rank capacity, bad rescaling): the general path handles it
+            consumed = nobs - host["nobs"]
+            host["nobs"], host["rank"] = nobs, int(hdr_c[0])
+            self._on_status(int(hdr_c[1]))
+            if consumed:
+                return UpdateReport("independent" if hdr_b[0] else "dependent", gain.copy(), float(resid[0]),
+                                    self.rank)
         out = self._run(row[None, :], np.array([target], dtype=self._kind.dtype), want_report=True)
         branch = "independent" if out["branch"][0] else "dependent"
         return UpdateReport(branch, out["gain"], float(out["resid"][0]), self.rank)
@@ -238,6 +262,23 @@ class RecursiveSolver:
         if A.shape[1] != self._m:
             raise ValueError(f"rows have {A.shape[1]} columns, expected {self._m}")
         y = self._kind.vector(targets, A.shape[0])
+        fast = self._fast.get(False) if self._fast else None
+        if A.shape[0] == 1 and fast is not None and fast[0] == self._st_key:
+            _, pin, run, h, s, hdr_n, hdr_c = fast[:7]
+            m = self._m
+            pin[:m] = A[0]
+            pin[m] = y[0]
+            rc = run(h, s)
+            if rc:
+                _lib.check(rc, "rgb_rowpipe_run")
+            nobs = int(hdr_n[0])
+            consumed = nobs - self._host["nobs"]
+            self._host["nobs"], self._host["rank"] = nobs, int(hdr_c[0])
+            if consumed and not hdr_c[1]:
+                return
+            self._on_status(int(hdr_c[1]))
+            if consumed:
+                return
         if A.shape[0]:
             self._run(A, y, want_report=False)
 
@@ -341,20 +382,24 @@ class RecursiveSolver:
         in_h, in_d = buf["in_h_p"], buf["in_d_p"]
         io_h, io_d = buf["io_h_p"], buf["io_d_p"]
         y_off = n * m  # the targets follow the rows in the staging block
-        if n == 1 and not self._trackers and self._graphs is not None:
-            # a per-row call: one replay of a captured copy-ingest-copy graph
-            g = self._row_graph(buf, want_report)
-            if g is not None:
-                buf["in_np"][:m] = A[0]
-                buf["in_np"][m] = y[0]
-                g.replay()
-                torch.cuda.current_stream(bs.device).synchronize()
-                consumed, status = self._take_counters(buf)
+        if n == 1 and not self._trackers and self._pipes is not None:
+            # a per-row call: the row pipe (one graph launch; the kernel reads the
+            # row from mapped host memory and writes the report back into it)
+            pipe = self._row_pipe(want_report)
+            if pipe is not None:
+                pipe["in"][:m] = A[0]
+                pipe["in"][m] = y[0]
+                _lib.check(lib.rgb_rowpipe_run(pipe["h"], pipe["stream"]), "rgb_rowpipe_run")
+                hdr = pipe["hdr"]
+                nobs, status = int(hdr["nobs"][0]), int(hdr["cnt"][1])
+                consumed = nobs - self._host["nobs"]
+                self._host["nobs"] = nobs
+                self._host["rank"] = int(hdr["cnt"][0])
                 if consumed:
                     self._on_status(status)
                     if want_report:
-                        return {"branch": buf["branch_np"][:1].copy(), "resid": buf["resid_np"][:1].copy(),
-                                "gain": buf["gain_np"].copy()}
+                        return {"branch": hdr["branch"].copy(), "resid": pipe["resid"].copy(),
+                                "gain": pipe["gain"].copy()}
                     return {}
                 self._on_status(status)  # rank cap: grown; the row runs again below
         stream = torch.cuda.current_stream(bs.device)
@@ -423,46 +468,66 @@ class RecursiveSolver:
             self._on_status(status)
         return res
 
-    def _row_graph(self, buf, want_report):
-        """CUDA graph of a one-row call -- host-to-device copy of the staged row
-        and target, rgb_ingest (T = 1, with the report logs for update()), and
-        the device-to-host copy of the counters and report -- captured once per
-        buffer and capacity layout, so update() costs one graph launch and one
-        synchronisation.  None (and graphs off) if capture fails."""
-        torch = self._torch
+    def _row_pipe(self, want_report):
+        """The librgb row pipe of this solver's current layout (include/rgb.h,
+        rgb_rowpipe_*): a graph captured once whose kernel reads the staged
+        row from pinned, device-mapped host memory and writes the report and
+        the counters back, so update() costs one graph launch and a spin on a
+        sequence word.  Recreated when the state moves (capacity growth).
+        None (and pipes off) if creation fails."""
         bs = self._bs
         cfg, st = self._structs()
-        key = (want_report, self._st_key, buf["in_d_p"], buf["io_d_p"])
-        g = self._graphs.get(key)
-        if g is not None:
-            return g
-        self._graphs.clear()  # a layout change invalidates the older graphs
-        m, esz = self._m, buf["esz"]
-        io_d = buf["io_d_p"]
-        logs = _lib.Logs(io_d + buf["off_branch"] if want_report else None, None,
-                         io_d + buf["off_resid"] if want_report else None,
-                         io_d + buf["off_gain"] if want_report else None)
-        ingest = bs.lib.rgb_ingest_f32in if self._f32in else bs.lib.rgb_ingest
-        cp = bs.lib.rgb_memcpy_async
-        nb = buf["off_resid"] + esz if want_report else 16
-        gs = torch.cuda.Stream(bs.device)
-        g = torch.cuda.CUDAGraph()
-        rcs = []
-        try:
-            with torch.cuda.graph(g, stream=gs, capture_error_mode="thread_local"):
-                h = ctypes.c_void_p(gs.cuda_stream)
-                rcs.append(cp(buf["in_d_p"], buf["in_h_p"], (m + 1) * esz, h))
-                rcs.append(ingest(ctypes.byref(cfg), ctypes.byref(st), buf["in_d_p"], m,
-                                  buf["in_d_p"] + m * esz, 1, 1, ctypes.byref(logs), h))
-                rcs.append(cp(buf["io_h_p"], io_d, nb, h))
-        except RuntimeError:
-            rcs.append(-1)
-        if any(rcs):
-            self._graphs = None
+        key = (want_report, self._st_key)
+        pipe = self._pipes.get(key)
+        if pipe is not None:
+            return pipe
+        self._drop_pipes(keep=self._st_key)  # pipes of an older layout point at freed buffers
+        lib = bs.lib
+        h, blk = ctypes.c_void_p(), ctypes.c_void_p()
+        # the device counters must be current before the pipe's first run
+        self._torch.cuda.current_stream(bs.device).synchronize()
+        if lib.rgb_rowpipe_create(ctypes.byref(cfg), ctypes.byref(st), int(want_report), int(self._f32in),
+                                  ctypes.byref(h), ctypes.byref(blk)) != _lib.OK:
+            self._pipes = None
             return None
-        g._rgb_keep = (logs, cfg, st)  # the captured launch read these structs
-        self._graphs[key] = g
-        return g
+        off = [ctypes.c_int64() for _ in range(3)]
+        nbytes = lib.rgb_rowpipe_layout(ctypes.byref(cfg), int(self._f32in), *[ctypes.byref(o) for o in off])
+        raw = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(blk.value))
+        sdt = np.dtype(np.float32 if bs.dtype == self._torch.float32 else np.float64)
+        idt = np.dtype(np.float32) if (self._f32in or sdt == np.float32) else np.dtype(np.float64)
+        o_in, o_res, o_gain = (o.value for o in off)
+        m = self._m
+        pipe = {"h": h, "raw": raw,
+                # every drop-in call completes before it returns, so one stream
+                # handle per pipe is safe
+                "stream": ctypes.c_void_p(self._torch.cuda.current_stream(bs.device).cuda_stream),
+                "in": raw[o_in:o_in + idt.itemsize * (m + 1)].view(idt),
+                "resid": raw[o_res:o_res + sdt.itemsize].view(sdt),
+                "gain": raw[o_gain:o_gain + sdt.itemsize * m].view(sdt),
+                "hdr": {"nobs": raw[_lib.ROWPIPE_OFF_NOBS:_lib.ROWPIPE_OFF_NOBS + 8].view(np.int64),
+                        "cnt": raw[_lib.ROWPIPE_OFF_RANK:_lib.ROWPIPE_OFF_STATUS + 4].view(np.int32),
+                        "branch": raw[_lib.ROWPIPE_OFF_BRANCH:_lib.ROWPIPE_OFF_BRANCH + 1]}}
+        self._pipes[key] = pipe
+        hdr = pipe["hdr"]
+        self._fast[want_report] = (self._st_key, pipe["in"], lib.rgb_rowpipe_run, h, pipe["stream"], hdr["nobs"],
+                                   hdr["cnt"], hdr["branch"], pipe["resid"], pipe["gain"])
+        return pipe
+
+    def _drop_pipes(self, keep=None):
+        """Destroy the row pipes (all, or those not of layout `keep`)."""
+        if self._fast:
+            for wr in [wr for wr, f in self._fast.items() if f[0] != keep]:
+                del self._fast[wr]
+        if self._pipes:
+            lib = self._bs.lib
+            for key in [key for key in self._pipes if key[1] != keep]:
+                lib.rgb_rowpipe_destroy(self._pipes.pop(key)["h"])
+
+    def __del__(self):
+        try:
+            self._drop_pipes()
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
 
     def _take_counters(self, buf):
         """Counters of the last report copy: records nobs and rank; returns
@@ -479,6 +544,7 @@ class RecursiveSolver:
         stop (invalid rescaling factor) raises."""
         bs = self._bs
         if status & _lib.ST_RANK_CAP:
+            self._drop_pipes()  # the state moves
             bs.grow(2 * bs.r_cap)
             bs.status_t.zero_()
         elif status:

@@ -20,7 +20,7 @@ def lib():
 
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "rgb.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(rgb_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|void|const char \*)\s*(rgb_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_exports():

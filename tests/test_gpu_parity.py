@@ -815,10 +815,12 @@ def test_dropin_solver_large_width_grows_capacity_on_the_grid_kernel():
 
 
 @pytest.mark.parametrize("variant", ["general", "orthogonal", "orthonormal"])
-def test_update_graph_replay_matches_direct_calls(variant):
-    """update() and one-row ingest() replay a captured CUDA graph (copy in,
-    rgb_ingest, copy out); the reports, ranks and x equal those of the direct
-    calls, across a capacity growth (32 -> 64, the graph re-captured)."""
+def test_update_row_pipe_matches_direct_calls(variant):
+    """update() and one-row ingest() run through the librgb row pipe (a graph
+    whose kernel reads the row from mapped host memory and writes the report
+    back); the reports, ranks and x equal those of the direct calls (staged
+    copies, rgb_ingest), bit for bit, across a capacity growth (32 -> 64, the
+    pipe re-created)."""
     from paper_2106_11594_b200 import RecursiveSolver
 
     rng = np.random.default_rng(4)
@@ -826,7 +828,7 @@ def test_update_graph_replay_matches_direct_calls(variant):
     rows = np.vstack([rng.standard_normal((40, m)), rng.standard_normal((60, 40)) @ rng.standard_normal((40, m))])
     ys = rng.standard_normal(100)
     solvers = [RecursiveSolver(m, variant=variant, alpha=2.0 if variant == "orthogonal" else 1) for _ in range(2)]
-    solvers[1]._graphs = None
+    solvers[1]._pipes = None
     for i in range(100):
         reps = [s.update(rows[i], ys[i]) for s in solvers] if i % 3 else \
             [s.ingest(rows[i:i + 1], ys[i:i + 1]) for s in solvers]
@@ -835,7 +837,7 @@ def test_update_graph_replay_matches_direct_calls(variant):
             assert a.branch == b.branch and a.new_rank == b.new_rank
             assert np.array_equal(a.gain, b.gain) and a.predicted_residual == b.predicted_residual
         assert solvers[0].rank == solvers[1].rank and solvers[0].num_observations == i + 1
-    assert solvers[0]._graphs, "the graph path did not run"
+    assert solvers[0]._pipes, "the row pipe did not run"
     assert np.array_equal(np.asarray(solvers[0].solution), np.asarray(solvers[1].solution))
     assert solvers[0].rank > 32
 
