@@ -176,9 +176,12 @@ typedef struct rgb_rowpipe rgb_rowpipe;
 int64_t rgb_rowpipe_layout(const rgb_config *cfg, int f32in, int64_t *off_in, int64_t *off_resid,
                            int64_t *off_gain);
 /* Capture the pipe for `state` (report logs when want_report); *host_block
- * receives the block the caller fills and reads. */
+ * receives the block the caller fills and reads.  host_x (optional, pinned
+ * host memory of m values of the state's type, cudaHostAlloc) receives the
+ * solution of the first right-hand side after every run -- the drop-in's
+ * live `solution` view (solver.py:200-202). */
 int rgb_rowpipe_create(const rgb_config *cfg, const rgb_state *state, int want_report, int f32in,
-                       rgb_rowpipe **pipe, void **host_block);
+                       void *host_x, rgb_rowpipe **pipe, void **host_block);
 /* Fold the row staged in the block; blocks until its report is visible. */
 int rgb_rowpipe_run(rgb_rowpipe *pipe, void *stream);
 void rgb_rowpipe_destroy(rgb_rowpipe *pipe);

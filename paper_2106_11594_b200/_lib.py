@@ -95,7 +95,7 @@ def load():
     lib.rgb_memcpy_async.argtypes = [vp, vp, i64, vp]
     i64p = ctypes.POINTER(ctypes.c_int64)
     lib.rgb_rowpipe_layout.argtypes = [cfgp, ctypes.c_int, i64p, i64p, i64p]
-    lib.rgb_rowpipe_create.argtypes = [cfgp, stp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp),
+    lib.rgb_rowpipe_create.argtypes = [cfgp, stp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp),
                                        ctypes.POINTER(vp)]
     lib.rgb_rowpipe_run.argtypes = [vp, vp]
     lib.rgb_rowpipe_destroy.argtypes = [vp]

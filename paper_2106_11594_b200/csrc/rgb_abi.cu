@@ -22,7 +22,7 @@ namespace rgb {
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms, bool f32in, unsigned char* mirror = nullptr,
-                   unsigned long long* dseq = nullptr);
+                   unsigned long long* dseq = nullptr, void* hx = nullptr);
 bool blocked_supports(const rgb_config& cfg);
 bool blocked_wg_supports(const rgb_config& cfg);
 bool panel_supports(const rgb_config& cfg);

@@ -109,7 +109,7 @@ template <typename REAL, typename TI>
 __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rows_stride,
     const TI* __restrict__ targets, int64_t tg_stride, int64_t T, rgb_logs logs, int cached,
-    unsigned char* __restrict__ mirror, unsigned long long* __restrict__ dseq) {
+    unsigned char* __restrict__ mirror, unsigned long long* __restrict__ dseq, REAL* __restrict__ hx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
   REAL* a_s = reinterpret_cast<REAL*>(smem_raw);        // m
@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(GEN_NT) generic_ingest_kernel(
       st.status[b] = status;
     }
     GENPROBE(6);
+    if (hx)  // row pipe: the solution (first right-hand side) into the caller's host mirror
+      for (int j = tid; j < m; j += GEN_NT) hx[j] = X[j];
     if (mirror) publish_row_report(mirror, dseq, nobs, r, status, tid);
     GENPROBE(7);
   }
@@ -369,7 +371,7 @@ static constexpr size_t GEN_CACHE_MAX = 96 * 1024;
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms, bool f32in, unsigned char* mirror,
-                   unsigned long long* dseq) {
+                   unsigned long long* dseq, void* hx) {
   if (cfg.k > GEN_MAX_K) return RGB_E_UNSUPPORTED;
   size_t smem = generic_smem_bytes(cfg);
   if (smem > 200 * 1024) return RGB_E_UNSUPPORTED;
@@ -381,18 +383,18 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
   if (cfg.dtype == RGB_F64 && f32in) {
     auto kern = generic_ingest_kernel<double, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                   (const float*)targets, tg_stride, T, logs, cached, mirror, dseq);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride, (const float*)targets,
+                                                   tg_stride, T, logs, cached, mirror, dseq, (double*)hx);
   } else if (cfg.dtype == RGB_F64) {
     auto kern = generic_ingest_kernel<double, double>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride,
-                                                   (const double*)targets, tg_stride, T, logs, cached, mirror, dseq);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const double*)rows, rows_stride, (const double*)targets,
+                                                   tg_stride, T, logs, cached, mirror, dseq, (double*)hx);
   } else {
     auto kern = generic_ingest_kernel<float, float>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride,
-                                                  (const float*)targets, tg_stride, T, logs, cached, mirror, dseq);
+    kern<<<(unsigned)grid, GEN_NT, smem, stream>>>(cfg, st, (const float*)rows, rows_stride, (const float*)targets,
+                                                  tg_stride, T, logs, cached, mirror, dseq, (float*)hx);
   }
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }

@@ -22,7 +22,7 @@ namespace rgb {
 int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
                    const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                    cudaStream_t stream, int num_sms, bool f32in, unsigned char* mirror = nullptr,
-                   unsigned long long* dseq = nullptr);
+                   unsigned long long* dseq = nullptr, void* hx = nullptr);
 
 
 // The row pipe's kernel: one row of one stream, the shape-generic kernel's
@@ -61,7 +61,7 @@ template <typename REAL>
 __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state st, const REAL* __restrict__ a_g,
                                                      const REAL* __restrict__ y_g, rgb_logs logs,
                                                      unsigned char* __restrict__ mirror,
-                                                     unsigned long long* __restrict__ dseq) {
+                                                     unsigned long long* __restrict__ dseq, REAL* __restrict__ hx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
   const bool onorm = var == RGB_ORTHONORMAL;
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
             REAL xv = X[(size_t)c * m + j];
             xv += g * dy(c);
             Xg[(size_t)c * m + j] = xv;
+            if (c == 0 && hx) hx[j] = xv;
           }
           if (gl) gl[j] = g;
         }
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
           REAL xv = X[(size_t)c * m + j];
           xv += g * dy(c);
           Xg[(size_t)c * m + j] = xv;
+          if (c == 0 && hx) hx[j] = xv;
         }
         if (gl) gl[j] = g;
       }
@@ -258,12 +260,13 @@ constexpr size_t R1_MAXS = 200 * 1024;
 
 template <typename REAL>
 static int launch_row1(const rgb_config& cfg, const rgb_state& st, const void* rows, const void* tgts,
-                       const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, cudaStream_t cs) {
+                       const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, void* hx,
+                       cudaStream_t cs) {
   const size_t smem = row1_smem(cfg);
   if (smem > R1_MAXS) return RGB_E_UNSUPPORTED;
   auto kern = row1_kernel<REAL>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq);
+  kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 }  // namespace rgb
@@ -275,6 +278,7 @@ struct rgb_rowpipe {
   unsigned char* host_dev = nullptr;  // its device alias
   unsigned long long* dseq = nullptr;
   unsigned long long seq = 0;
+  void* hx_dev = nullptr;  // caller's host x mirror (device alias), or null
   rgb_config cfg;
   rgb_state st;
   rgb_logs logs;
@@ -307,8 +311,8 @@ void rgb_rowpipe_destroy(rgb_rowpipe* p) {
   delete p;
 }
 
-int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_report, int f32in, rgb_rowpipe** out,
-                       void** host_block) {
+int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_report, int f32in, void* host_x,
+                       rgb_rowpipe** out, void** host_block) {
   if (!cfg || !st || !out || !host_block) return RGB_E_INVALID;
   if (cfg->num_streams != 1) return RGB_E_INVALID;  // one stream (the drop-in solver)
   *out = nullptr;
@@ -322,6 +326,7 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
   if (cfg->variant == RGB_ORTHONORMAL) p->st.dual = p->st.basis;
   cudaError_t e = cudaHostAlloc(&p->host, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable);
   if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&p->host_dev, p->host, 0);
+  if (e == cudaSuccess && host_x) e = cudaHostGetDevicePointer(&p->hx_dev, host_x, 0);
   if (e == cudaSuccess) e = cudaMalloc(&p->dseq, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(p->dseq, 0, sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -353,11 +358,11 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
     rc = RGB_E_UNSUPPORTED;
     if (!f32in && cfg->k <= rgb::R1_MK)
       rc = cfg->dtype == RGB_F64
-               ? rgb::launch_row1<double>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, cs)
-               : rgb::launch_row1<float>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, cs);
+               ? rgb::launch_row1<double>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, p->hx_dev, cs)
+               : rgb::launch_row1<float>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, p->hx_dev, cs);
     if (rc == RGB_E_UNSUPPORTED)  // float rows into a double state, k > 64, states beyond shared memory
       rc = rgb::launch_generic(p->cfg, p->st, rows, cfg->m, tgts, cfg->k, 1, p->logs, cs, nsm,
-                               f32in && cfg->dtype == RGB_F64, p->host_dev, p->dseq);
+                               f32in && cfg->dtype == RGB_F64, p->host_dev, p->dseq, p->hx_dev);
     e = cudaStreamEndCapture(cs, &p->graph);
   }
   if (e == cudaSuccess && rc == RGB_OK) e = cudaGraphInstantiate(&p->exec, p->graph, 0);

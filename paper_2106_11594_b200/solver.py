@@ -12,7 +12,8 @@ GPU and every update running in librgb.so (a one-stream ``BatchedSolver``):
   solve_batch(matrix, targets, ...) -> (x, rank)                   solver.py:406-422
 
 Differences, all deliberate and documented in DESIGN.md:
-  * ``solution`` and ``basis()`` return read-only host copies, not live views;
+  * ``solution`` is a live read-only view as in the reference, but of a pinned
+    host mirror that each call refreshes; ``basis()`` returns read-only copies;
   * RATIONAL (exact mode) and callable ``alpha`` are CPU-only features of the
     reference and raise CapabilityError here;
   * the stored rank has a device capacity that doubles on demand, so streams
@@ -142,6 +143,9 @@ class RecursiveSolver:
         self._torch = torch
         self._f32in = False
         self._host = {"rank": 0, "nobs": 0}
+        # pinned host mirror of x (first right-hand side): the live `solution` view
+        self._xh = torch.zeros(self._m, dtype=tdtype, pin_memory=True)
+        self._x_np = self._xh.numpy()
         self._pipes = {}  # one-row pipes (librgb rgb_rowpipe), by layout; None: unsupported
         self._fast = {}   # want_report -> the current pipe's handles, unpacked for update() / ingest()
 
@@ -172,8 +176,13 @@ class RecursiveSolver:
 
     @property
     def solution(self):
-        """Read-only host copy of the current minimum-norm solution."""
-        return _readonly(self._bs.x_t[0, 0].cpu().numpy())
+        """Live read-only view of the current minimum-norm solution
+        (solver.py:200-202): a view of a pinned host mirror that every call
+        refreshes (the row pipe's kernel writes it directly), so a view taken
+        earlier follows later updates, as the reference's does."""
+        v = self._x_np.view()
+        v.flags.writeable = False
+        return v
 
     def basis(self):
         """Read-only host copies of (C, C_tilde, P_inv)."""
@@ -432,6 +441,7 @@ class RecursiveSolver:
                 _lib.check(ingest(ctypes.byref(cfg), ctypes.byref(st), in_d + s0 * m * esz, 0,
                                   in_d + (y_off + s0) * esz, 0, s1 - s0, None, h), "rgb_ingest")
             _lib.check(cp(io_h, io_d, 16, h), "rgb_memcpy_async")
+            _lib.check(cp(self._xh.data_ptr(), bs.x_t.data_ptr(), m * esz, h), "rgb_memcpy_async")  # live view
             stream.synchronize()
             done, status = self._take_counters(buf)
             self._on_status(status)
@@ -456,6 +466,7 @@ class RecursiveSolver:
             # counters (and the report): one asynchronous copy into pinned memory, one sync
             nb = buf["off_resid"] + T * esz if want_report else 16
             _lib.check(cp(io_h, io_d, nb, h), "rgb_memcpy_async")
+            _lib.check(cp(self._xh.data_ptr(), bs.x_t.data_ptr(), m * esz, h), "rgb_memcpy_async")  # live view
             stream.synchronize()
             consumed, status = self._take_counters(buf)
             if log_coords and consumed:
@@ -487,7 +498,7 @@ class RecursiveSolver:
         # the device counters must be current before the pipe's first run
         self._torch.cuda.current_stream(bs.device).synchronize()
         if lib.rgb_rowpipe_create(ctypes.byref(cfg), ctypes.byref(st), int(want_report), int(self._f32in),
-                                  ctypes.byref(h), ctypes.byref(blk)) != _lib.OK:
+                                  ctypes.c_void_p(self._xh.data_ptr()), ctypes.byref(h), ctypes.byref(blk)) != _lib.OK:
             self._pipes = None
             return None
         off = [ctypes.c_int64() for _ in range(3)]

@@ -1255,3 +1255,27 @@ def test_pinv_and_covariance_at_the_config5_batch():
         assert relerr(pinv[b].cpu().numpy(), po) <= 1e-9
         assert relerr(V[b].cpu().numpy(), po @ po.T) <= 1e-9
         assert relerr(pinv[b].cpu().numpy(), np.linalg.pinv(A, rcond=1e-10)) <= 1e-8
+
+
+def test_solution_is_a_live_read_only_view():
+    """solution is a live read-only view (solver.py:200-202, test_solver.py:225-233):
+    writes raise ValueError, and a view taken earlier follows later update(),
+    one-row ingest() and block ingest() calls, bit for bit with a fresh read."""
+    import paper_2106_11594_b200 as p
+
+    rng = np.random.default_rng(12)
+    m = 48
+    A = rng.standard_normal((10, 6)) @ rng.standard_normal((6, m))
+    y = rng.standard_normal(10)
+    s = p.RecursiveSolver(m)
+    view = s.solution
+    with pytest.raises(ValueError):
+        view[0] = 1.0
+    assert not view.any()
+    s.update(A[0], y[0])
+    assert np.array_equal(view, s.solution) and view.any()
+    s.ingest(A[1:2], y[1:2])
+    s.ingest(A[2:], y[2:])
+    o = oracle.ingest(A[None], y[None], r_cap=m)
+    assert np.array_equal(view, s.solution)
+    assert relerr(view, oracle.solution(o)[0, :, 0]) <= 1e-12
