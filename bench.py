@@ -163,7 +163,8 @@ class ClockSampler:
 
 
 def fp64_peak():
-    """Live fp64 peaks of this GPU (tools/libfp64peak.so): DFMA and DMMA TFLOP/s."""
+    """Live peaks of this GPU (tools/libfp64peak.so), TFLOP/s: fp64 DFMA and DMMA,
+    and fp32 FFMA (the fp32-state kernel's pipe)."""
     import ctypes
 
     from paper_2106_11594_b200 import _build
@@ -171,7 +172,8 @@ def fp64_peak():
     try:
         lib = ctypes.CDLL(_build.build_peak_probe())
         lib.rgb_probe_fp64_peak.restype = ctypes.c_double
-        return {"dfma": lib.rgb_probe_fp64_peak(0), "dmma": lib.rgb_probe_fp64_peak(1)}
+        return {"dfma": lib.rgb_probe_fp64_peak(0), "dmma": lib.rgb_probe_fp64_peak(1),
+                "ffma": lib.rgb_probe_fp64_peak(2)}
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)}
 
@@ -472,11 +474,19 @@ def run_ours(args):
         r_np, t_np = rows[:ns].cpu().numpy(), tg[:ns].cpu().numpy()
         o = oracle.ingest(r_np.astype(np.float64), t_np.astype(np.float64), r_cap=cfg.r_cap, eps=args.eps,
                           nthreads=8, logs=False)
-        x = bs.solution[:ns].cpu().numpy()
+        x = bs.solution[:ns].cpu().numpy().astype(np.float64)
         xo = oracle.solution(o)
         ok = (o["status"] == 0) & (status[:ns] == 0)
+        rank_ref = o["rank"]
+        if args.dtype == "fp32-state":
+            # fp32 policy: ranks against the oracle's fp32 mode on the
+            # same float32 bytes; x against the fp64 oracle within 1e-3 where the
+            # fp32 and fp64 oracle ranks agree
+            o32 = oracle.ingest(r_np, t_np, r_cap=cfg.r_cap, eps=args.eps, dtype=np.float32, nthreads=8, logs=False)
+            ok &= (o32["status"] == 0) & (o32["rank"] == o["rank"])
+            rank_ref = o32["rank"]
         errs = [float(np.abs(x[b] - xo[b]).max() / max(1.0, np.abs(xo[b]).max())) for b in range(ns) if ok[b]]
-        parity = {"streams": ns, "rank_match": bool(np.array_equal(ranks[:ns][ok], o["rank"][ok])),
+        parity = {"streams": ns, "rank_match": bool(np.array_equal(ranks[:ns][ok], rank_ref[ok])),
                   "x_relerr_max": max(errs) if errs else None,
                   "tolerance": 1e-3 if args.dtype == "fp32-state" else 1e-9}
         # streams the device froze at the rank capacity: the oracle, given room
@@ -510,7 +520,7 @@ def run_ours(args):
         peak_tf = peaks.get("dmma")
         peak_src = "live fp64 DMMA m8n8k4 probe (tools/fp64_peak.cu), this GPU, this run"
         if args.dtype == "fp32-state":
-            peak_tf, peak_src = 2 * peaks.get("dfma", 0), "2x live fp64 DFMA probe (fp32 FMA rate)"
+            peak_tf, peak_src = peaks.get("ffma"), "live fp32 FFMA probe (tools/fp64_peak.cu), this GPU, this run"
         achieved = flops_total / world / (kern_ms * 1e-3) / 1e12
         byt = alg_bytes(S, n, cfg.m, cfg.k, esize, 4 if args.dtype == "fp32-state" else 8)
         hbm_gbs = byt / (kern_ms * 1e-3) / 1e9
@@ -530,15 +540,17 @@ def run_ours(args):
                               f"inputs {byt * world / 1e9:.1f} GB >> L2 126 MB (no flush needed)"),
                        "sharding": (f"{S} contiguous streams per GPU of {B}, no collective" if cfg.streams > 1 else
                                     "single stream: one replica per GPU (rows are sequential; replicas only)")},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+            "roofline": {"bound": "compute" if args.dtype == "fp32-state" else "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf if peak_tf else None,
                          "traffic": ncu_traffic(args.config, args.dtype),
                          "algorithmic_flops_per_launch": flops_total / world,
                          "kernel_ms": kern_ms, "peak_source": peak_src,
-                         "note": ("bound by the fp64 tensor pipe (mma.sync DMMA; tcgen05 has no f64 kind); achieved "
-                                  "counts the reference's per-row op count (SURVEY.md 8(d)) over the branch log -- "
-                                  "the blocked algebra executes ~65% of it as MMAs, so frac can exceed the DMMA "
-                                  "pipe utilisation ncu reports (profiles/)"),
+                         "note": (("bound by the fp32 CUDA-core pipe (FFMA; the fp32-state kernel rgb_f32.cu); "
+                                   if args.dtype == "fp32-state" else
+                                   "bound by the fp64 tensor pipe (mma.sync DMMA; tcgen05 has no f64 kind); ") +
+                                  "achieved counts the reference's per-row op count (SURVEY.md 8(d)) over the branch "
+                                  "log -- the blocked algebra executes ~65% of it, so frac can exceed the pipe "
+                                  "utilisation ncu reports (profiles/)"),
                          "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": mp.get("hbm_gbs"),
                                  "frac": hbm_gbs / mp["hbm_gbs"] if mp.get("hbm_gbs") else None,
                                  "algorithmic_bytes_per_launch": byt}},

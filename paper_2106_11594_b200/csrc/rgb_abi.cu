@@ -29,6 +29,9 @@ bool panel_supports(const rgb_config& cfg);
 int launch_panel(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
                  int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms, bool f32in);
 bool grid_supports(const rgb_config& cfg);
+bool f32_supports(const rgb_config& cfg);
+int launch_f32(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
+               int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms);
 bool cluster_supports(const rgb_config& cfg);
 int launch_cluster(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride, const void* targets,
                    int64_t tg_stride, int64_t T, const rgb_logs& logs, cudaStream_t stream, int num_sms,
@@ -151,7 +154,10 @@ static int ingest_impl(const rgb_config* cfg, rgb_state* st, const void* rows, i
   const int nsm = sm_count();
   if (cfg->dtype == RGB_F32) f32in = false;  // the inputs already have the state's type
   rc = RGB_E_UNSUPPORTED;
-  if (rgb::blocked_supports(*cfg) && !lg.resid && !lg.gain)
+  if (rgb::f32_supports(*cfg) && !lg.resid && !lg.gain && !env_flag("RGB_NO_F32K"))
+    rc = rgb::launch_f32(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm);
+  if (rc != RGB_E_UNSUPPORTED) {
+  } else if (rgb::blocked_supports(*cfg) && !lg.resid && !lg.gain)
     rc = rgb::launch_blocked(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);
   else if (rgb::panel_supports(*cfg) && !lg.resid && !lg.gain && !env_flag("RGB_NO_PANEL"))
     rc = rgb::launch_panel(*cfg, s2, rows, rows_stride, targets, targets_stride, T, lg, s, nsm, f32in);

@@ -16,12 +16,12 @@ import sys
 import tempfile
 
 
-def sass_samples(path):
+def sass_samples(path, column="Warp Stall Sampling (All Samples)"):
     rows = list(csv.reader(open(path)))
     kname = rows[0][1] if len(rows[0]) > 1 else ""
     h = rows[1]
     ia, isrc = h.index("Address"), h.index("Source")
-    iall = h.index("Warp Stall Sampling (All Samples)")
+    iall = h.index(column)
     data = [(int(r[ia], 16), r[isrc].strip(), float(r[iall] or 0)) for r in rows[2:] if r[ia].startswith("0x")]
     base = data[0][0]
     return kname, [(a - base, s, n) for a, s, n in data]
@@ -56,7 +56,8 @@ def line_map(so, kernel_sub):
 def main():
     csvp, so, sub = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    kname, samples = sass_samples(csvp)
+    # RGB_NCU_COLUMN="Instructions Executed" ranks lines by executed instructions instead
+    kname, samples = sass_samples(csvp, os.environ.get("RGB_NCU_COLUMN", "Warp Stall Sampling (All Samples)"))
     cands, maps = line_map(so, sub)
     # pick the candidate whose instruction count matches the sampled kernel
     best = max(cands, key=lambda k: -abs(len(maps[k]) - len(samples)))
