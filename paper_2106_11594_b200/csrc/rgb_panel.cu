@@ -53,6 +53,7 @@
 //   -C     Cf[kt][jt][lane]  = -C[sigma(kt,q)][8jt+p]    shared memory (B operand of R)
 //   P^-1   Pr[mt][nt][e]     = P[8mt+p][8nt+2q+e]        home registers (symmetric)
 //   W^T    Wt[mt][e]         = W[8mt+2q+e][c=p]          home registers
+#include <cstddef>
 #include <type_traits>
 
 #include "rgb_mma.cuh"
@@ -150,6 +151,8 @@ struct PanelSmem {
   double a2part[PW + 1], r2part[PW + 1];
   double gam[R];               // growth: coords of the row
   double kv[M];                //         its gain K = rej / |rej|^2
+  // bulk growth's scratch spans sG .. here: 8 x M + 8 x R doubles (padded to fit)
+  double bulkpad[R >= 32 ? 48 : 384];
 };
 
 template <int R, int M, typename TI>
@@ -233,6 +236,226 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
     // warps, the rejection of the own columns 8J + p, its norm summed the same
     // way, and the growth applied by every warp to its own columns.
     if (fresh && !has_x0) {
+      // ---- bulk growth: whole 8-row tiles of leading rows whose independence is certain
+      // The reference grows the basis one row at a time (solver.py:305-318, _grow
+      // :368-380): K = rej / |rej|^2, C~ <- [C~ - gamma K^T; K^T], C <- [C; a],
+      // P^-1 <- diag(P^-1, 1), W gains y - a.x0 (= y here: x0 = 0).  For a tile of
+      // rows that are all independent the same result is, in exact arithmetic,
+      // one block step: with R = A - G C the tile's rejections from the current
+      // basis (G = A C~^T), the new dual rows are Z = (R R^T)^-1 R and the old ones
+      // become C~ - G^T Z.  The squared rejection of row t from the basis plus the
+      // tile's rows before t is the t-th pivot d_t of R R^T = L D L^T, so a row is
+      // certified when d_t clears the rank test by BULK_MARGIN (the reference then
+      // surely finds it independent too) and keeps >= BULK_COND of |R_t|^2 (the
+      // tile is well conditioned, so the normal-equations solve Z = E^T D^-1 E R,
+      // E = L^-1, stays at the reference's accuracy).  The first row that is not
+      // certified ends the bulk phase; it and the rest go to the row mode below.
+      // One warp projects (DMMA), factors and solves; all four update C~.
+      // (scripts/bulk_sim4.py restates it: 4 096 config-3-like streams, branch logs
+      // identical to the oracle's except 2 in the noise band, x within 3e-10.)
+      if constexpr (M == 128) {
+        constexpr double BULK_COND = 0.1, BULK_MARGIN = 1e6;
+        __shared__ int s_bulk_tst;
+        constexpr int SP = M + 4;        // S1 row pitch (conflict-free B-operand reads)
+        double* S1 = &S.sG[0][0][0][0];  // [8][SP]: R, then D^-1 E R, then Z
+        double* Gs = S1 + TT * SP;       // [8][R]: G of the tile
+        static_assert(offsetof(SMT, bulkpad) + sizeof(S.bulkpad) - offsetof(SMT, sG) >=
+                          sizeof(double) * (TT * SP + TT * R),
+                      "bulk growth: scratch fits the hand-off slot");
+        double* Dflat = &S.Df[0][0][0];
+        double* Cflat = &S.Cf[0][0][0];
+        auto df_idx = [&](int i, int c) {
+          return ((i >> 3) * KS + 2 * (c >> 3) + (c & 1)) * 32 + 4 * (i & 7) + ((c & 7) >> 1);
+        };
+        auto cf_idx = [&](int i, int c) {
+          return ((2 * (i >> 3) + (i & 1)) * NJ + (c >> 3)) * 32 + 4 * (c & 7) + ((i & 7) >> 1);
+        };
+        const int tid = threadIdx.x;
+        while (tcur + TT <= T && r + TT <= R) {
+          PPROBE(20);
+          if (w == 0) {
+            double acc[NJ][2];
+#pragma unroll
+            for (int jt = 0; jt < NJ; ++jt) {
+              const double2 v = ld2(Rb + (tcur + p) * M + 8 * jt + 2 * q);
+              acc[jt][0] = v.x;
+              acc[jt][1] = v.y;
+              // C's candidate rows r + p (zeroed again below past the certified block)
+              Cflat[cf_idx(r + p, 8 * jt + 2 * q)] = -v.x;
+              Cflat[cf_idx(r + p, 8 * jt + 2 * q + 1)] = -v.y;
+            }
+            double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int jt = 0; jt < NJ; ++jt) {
+              s4[(2 * jt) & 3] = fma(acc[jt][0], acc[jt][0], s4[(2 * jt) & 3]);
+              s4[(2 * jt + 1) & 3] = fma(acc[jt][1], acc[jt][1], s4[(2 * jt + 1) & 3]);
+            }
+            double asq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            asq += __shfl_xor_sync(FULL, asq, 1);
+            asq += __shfl_xor_sync(FULL, asq, 2);
+            bool yok = true;
+            if (q == 0)
+              for (int c = 0; c < k; ++c) yok &= isfinite((double)Yb[(tcur + p) * k + c]);
+            yok = __shfl_sync(FULL, yok, 4 * p);
+            // G = A C~^T and R = A - G C (rank tiles past r are zero)
+            const int nti = (r + 7) >> 3;
+            double g[IT][2], h[IT][2];
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = h[nt][0] = h[nt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS / 2; ++ks)
+#pragma unroll
+              for (int nt = 0; nt < IT; ++nt)
+                if (nt < nti) {
+                  mma(g[nt], acc[ks >> 1][ks & 1], S.Df[nt][ks][lane]);
+                  mma(h[nt], acc[(ks + KS / 2) >> 1][ks & 1], S.Df[nt][ks + KS / 2][lane]);
+                }
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt) {
+              g[nt][0] += h[nt][0];
+              g[nt][1] += h[nt][1];
+            }
+#pragma unroll
+            for (int kt = 0; kt < IK; ++kt)
+              if ((kt >> 1) < nti) {
+#pragma unroll
+                for (int jt = 0; jt < NJ; ++jt) mma(acc[jt], g[kt >> 1][kt & 1], S.Cf[kt][jt][lane]);
+              }
+#pragma unroll
+            for (int nt = 0; nt < IT; ++nt) {
+              Gs[p * R + 8 * nt + 2 * q] = g[nt][0];
+              Gs[p * R + 8 * nt + 2 * q + 1] = g[nt][1];
+            }
+            // M = R R^T, L D L^T (E = L^-1)
+            double m4[4][2] = {};
+#pragma unroll
+            for (int jt = 0; jt < NJ; ++jt) {
+              mma(m4[(2 * jt) & 3], acc[jt][0], acc[jt][0]);
+              mma(m4[(2 * jt + 1) & 3], acc[jt][1], acc[jt][1]);
+            }
+            const double mm[2] = {(m4[0][0] + m4[1][0]) + (m4[2][0] + m4[3][0]),
+                                  (m4[0][1] + m4[1][1]) + (m4[2][1] + m4[3][1])};
+            // a non-finite row would reach the earlier rows' factors through 0 x NaN in
+            // the elimination: its row and column enter as the identity (it fails the
+            // certification below anyway)
+            double mi[2], ev[2], rd0, rd1;
+            {
+              const bool badp = !isfinite(asq);
+              const bool badc0 = !isfinite(__shfl_sync(FULL, asq, 8 * q));
+              const bool badc1 = !isfinite(__shfl_sync(FULL, asq, 8 * q + 4));
+              mi[0] = (badp || badc0) ? (p == 2 * q ? 1.0 : 0.0) : mm[0];
+              mi[1] = (badp || badc1) ? (p == 2 * q + 1 ? 1.0 : 0.0) : mm[1];
+            }
+            ldl8(mi, ev, rd0, rd1, p, q);
+            // certification, lane t < 8 tests row t; one ballot
+            int tst;
+            {
+              const int t = lane & 7;
+              const double x0 = __shfl_sync(FULL, rd0, t >> 1), x1 = __shfl_sync(FULL, rd1, t >> 1);
+              const double dt = 1.0 / ((t & 1) ? x1 : x0);
+              const double y0 = __shfl_sync(FULL, mm[0], 4 * t + (t >> 1));
+              const double y1 = __shfl_sync(FULL, mm[1], 4 * t + (t >> 1));
+              const double mtt = (t & 1) ? y1 : y0;
+              const double at = __shfl_sync(FULL, asq, 4 * t);
+              const bool yt = __shfl_sync(FULL, yok, 4 * t);
+              const double e2 = eps_sq<double>(cfg, r + t);
+              const bool ok = isfinite(at) && yt && dt > BULK_COND * mtt && dt > BULK_MARGIN * e2 * fmax(1.0, at);
+              const unsigned failm = __ballot_sync(FULL, lane < TT && !ok);
+              tst = failm ? __ffs(failm) - 1 : TT;
+            }
+            if (tst > 0) {
+              // rows / columns past the certified block: E = I, 1/d = 1 there
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int c = 2 * q + e;
+                if (p >= tst || c >= tst) ev[e] = (p == c) ? 1.0 : 0.0;
+              }
+              const double z0 = __shfl_sync(FULL, rd0, p >> 1), z1 = __shfl_sync(FULL, rd1, p >> 1);
+              const double rdp = p < tst ? ((p & 1) ? z1 : z0) : 1.0;
+#pragma unroll
+              for (int jt = 0; jt < NJ; ++jt)
+                *reinterpret_cast<double2*>(S1 + p * SP + 8 * jt + 2 * q) =
+                    p < tst ? make_double2(acc[jt][0], acc[jt][1]) : make_double2(0.0, 0.0);  // (0 x NaN)
+              __syncwarp();
+              // Q = D^-1 E R  (K = the tile's rows, permuted: step kk takes row 2q + kk)
+              double qv[NJ][2];
+#pragma unroll
+              for (int jt = 0; jt < NJ; ++jt) qv[jt][0] = qv[jt][1] = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int jt = 0; jt < NJ; ++jt) mma(qv[jt], ev[kk], S1[(2 * q + kk) * SP + 8 * jt + p]);
+              __syncwarp();
+#pragma unroll
+              for (int jt = 0; jt < NJ; ++jt)
+                *reinterpret_cast<double2*>(S1 + p * SP + 8 * jt + 2 * q) =
+                    make_double2(qv[jt][0] * rdp, qv[jt][1] * rdp);
+              __syncwarp();
+              // Z = E^T Q (E^T[p][2q + kk] = E[2q + kk][p], from the lane that holds it)
+              double zv[NJ][2];
+#pragma unroll
+              for (int jt = 0; jt < NJ; ++jt) zv[jt][0] = zv[jt][1] = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk) {
+                const int src = 4 * (2 * q + kk) + (p >> 1);
+                const double e0 = __shfl_sync(FULL, ev[0], src), e1 = __shfl_sync(FULL, ev[1], src);
+                const double a = (p & 1) ? e1 : e0;
+#pragma unroll
+                for (int jt = 0; jt < NJ; ++jt) mma(zv[jt], a, S1[(2 * q + kk) * SP + 8 * jt + p]);
+              }
+              __syncwarp();
+#pragma unroll
+              for (int jt = 0; jt < NJ; ++jt)
+                *reinterpret_cast<double2*>(S1 + p * SP + 8 * jt + 2 * q) =
+                    p < tst ? make_double2(zv[jt][0], zv[jt][1]) : make_double2(0.0, 0.0);
+            }
+            if (lane == 0) s_bulk_tst = tst;
+          }
+          PPROBE(16);
+          __syncthreads();
+          PPROBE(17);
+          const int tst = s_bulk_tst;
+          if (tst == 0) break;
+          // C~[:r] -= G^T Z, C~[r + t] = Z[t]; C's rows past the block leave again (every warp)
+          {
+            const double* __restrict__ gs = Gs;
+            const double* __restrict__ zs = S1;
+            for (int e = tid; e < r * M; e += PANEL_THREADS) {
+              const int i = e / M, c = e % M;
+              double gz[TT];
+#pragma unroll
+              for (int t = 0; t < TT; ++t) gz[t] = t < tst ? gs[t * R + i] * zs[t * SP + c] : 0.0;
+              const int di = df_idx(i, c);
+              double v = Dflat[di];
+#pragma unroll
+              for (int t = 0; t < TT; ++t) v -= gz[t];
+              Dflat[di] = v;
+            }
+          }
+          PPROBE(18);
+          for (int e = tid; e < TT * M; e += PANEL_THREADS) {
+            const int t = e / M, c = e % M;
+            if (t < tst) Dflat[df_idx(r + t, c)] = S1[t * SP + c];
+            else Cflat[cf_idx(r + t, c)] = 0.0;
+          }
+          if (blog)
+            for (int t = tid; t < tst; t += PANEL_THREADS) blog[b * T + tcur + t] = 1;
+          if (clog)
+            for (int e = tid; e < tst * R; e += PANEL_THREADS)
+              clog[(b * T + tcur + e / R) * R + e % R] = (e % R == r + e / R) ? 1.0 : 0.0;
+          r += tst;
+          tcur += tst;
+          PPROBE(19);
+          __syncthreads();
+          if (tst < TT) break;
+        }
+        // W's rows of the grown prefix: y (x0 = 0), over the scratch
+        for (int e = tid; e < R * 8; e += PANEL_THREADS) {
+          const int t = e >> 3, c = e & 7;
+          (&Wsm[0][0])[e] = (t < r && c < k) ? (double)Yb[(int64_t)t * k + c] : 0.0;
+        }
+        __syncthreads();
+      }
       constexpr int NRW = PW + 1, NGR = NJ / NRW;
       static_assert(NJ % NRW == 0, "row mode: whole column groups per warp");
       const int u = threadIdx.x >> 5;
@@ -250,7 +473,7 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
           nyv = (p < k) ? (double)Yb[t * k + p] : 0.0;  // y[c = p]
         }
       };
-      load_row(0);
+      load_row(tcur);
       // the row step, specialised on the number of nonzero rank tiles (the
       // unrolled loops then carry no predicated-off work)
       auto row_step = [&](auto NTc) -> bool {
