@@ -64,5 +64,34 @@ __device__ __forceinline__ double rcp64(double x) {
   return fma(r, e, r);
 }
 
+// 8x8 LDL^T of the SPD matrix M (accumulator layout mi[e] = M[p][2q+e]):
+// ev[e] = E[p][2q+e] with E = L^-1, rd0 / rd1 = 1/d at t = 2q, 2q+1.
+__device__ __forceinline__ void ldl8(double (&mi)[2], double (&ev)[2], double& rd0, double& rd1, int p, int q) {
+  // Gaussian elimination in registers, the same steps as the other blocked
+  // kernels (a fraction-free variant without the reciprocal on the chain and a
+  // one-Newton-step reciprocal were both measured slower here).
+  ev[0] = p == 2 * q ? 1.0 : 0.0;
+  ev[1] = p == 2 * q + 1 ? 1.0 : 0.0;
+#pragma unroll
+  for (int kk = 0; kk < TT - 1; ++kk) {
+    const double v = (kk & 1) ? mi[1] : mi[0];
+    const double piv = __shfl_sync(FULL, v, 4 * kk + (kk >> 1));
+    const double mps = __shfl_sync(FULL, v, 4 * p + (kk >> 1));
+    const double m0 = __shfl_sync(FULL, mi[0], 4 * kk + q);
+    const double m1 = __shfl_sync(FULL, mi[1], 4 * kk + q);
+    const double e0 = __shfl_sync(FULL, ev[0], 4 * kk + q);
+    const double e1 = __shfl_sync(FULL, ev[1], 4 * kk + q);
+    const double f = (p > kk) ? mps * rcp64(piv) : 0.0;
+    mi[0] = fma(-f, m0, mi[0]);
+    mi[1] = fma(-f, m1, mi[1]);
+    ev[0] = fma(-f, e0, ev[0]);
+    ev[1] = fma(-f, e1, ev[1]);
+  }
+  const double dsel0 = (p & 1) ? mi[1] : mi[0];
+  const double rd_ = rcp64(__shfl_sync(FULL, dsel0, 4 * p + (p >> 1)));
+  rd0 = __shfl_sync(FULL, rd_, 8 * q);
+  rd1 = __shfl_sync(FULL, rd_, 8 * q + 4);
+}
+
 }  // namespace blk
 }  // namespace rgb
