@@ -42,7 +42,6 @@ struct __align__(16) WarpSmem {
   float P[R][PS];       // P^-1
   float Wt[KX][PS];     // W^T (W: R x k)
   float Us[TT][PS];     // U = G P (t x i)
-  float Mm[TT][TT];     // I + S, eliminated in place
   float Em[TT][TT];     // E = L^-1
   float Yy[R][TT];      // Y = U^T E^T (i x t)
   float Dy[TT][KX];     // dy0
@@ -67,6 +66,33 @@ __device__ __forceinline__ void cp4(void* smem, const void* gmem, bool ok) {
 __device__ __forceinline__ void cp16(void* smem, const void* gmem, bool ok) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(ok ? 16 : 0));
+}
+
+// 8x8 L D L^T of the SPD matrix M in registers (lane = 4p + q holds M[p][2q + e]):
+// ev[e] = E[p][2q + e] with E = L^-1; rd0 / rd1 = 1/d at t = 2q, 2q + 1.  The
+// float32 restatement of rgb_mma.cuh's ldl8 (Gaussian elimination by shuffles).
+__device__ __forceinline__ void ldl8f(float (&mi)[2], float (&ev)[2], float& rd0, float& rd1, int p, int q) {
+  ev[0] = p == 2 * q ? 1.f : 0.f;
+  ev[1] = p == 2 * q + 1 ? 1.f : 0.f;
+#pragma unroll
+  for (int kk = 0; kk < TT - 1; ++kk) {
+    const float v = (kk & 1) ? mi[1] : mi[0];
+    const float piv = __shfl_sync(FULL, v, 4 * kk + (kk >> 1));
+    const float mps = __shfl_sync(FULL, v, 4 * p + (kk >> 1));
+    const float m0 = __shfl_sync(FULL, mi[0], 4 * kk + q);
+    const float m1 = __shfl_sync(FULL, mi[1], 4 * kk + q);
+    const float e0 = __shfl_sync(FULL, ev[0], 4 * kk + q);
+    const float e1 = __shfl_sync(FULL, ev[1], 4 * kk + q);
+    const float f = (p > kk) ? mps * rcpf(piv) : 0.f;
+    mi[0] = fmaf(-f, m0, mi[0]);
+    mi[1] = fmaf(-f, m1, mi[1]);
+    ev[0] = fmaf(-f, e0, ev[0]);
+    ev[1] = fmaf(-f, e1, ev[1]);
+  }
+  const float dsel = (p & 1) ? mi[1] : mi[0];
+  const float rdp = rcpf(__shfl_sync(FULL, dsel, 4 * p + (p >> 1)));
+  rd0 = __shfl_sync(FULL, rdp, 8 * q);
+  rd1 = __shfl_sync(FULL, rdp, 8 * q + 4);
 }
 
 // Reduce-scatter of N values (N = 32 or 16 per half-warp) across the lanes:
@@ -98,10 +124,19 @@ __device__ __forceinline__ void stage_tile(WarpSmem& S, int s, const float* rows
     const bool ok = t0 + t < T;
     cp16(&S.A[s][t][c4], ok ? rows + (t0 + t) * M + c4 : rows, ok);
   }
-  for (int e = lane; e < TT * KX; e += 32) {
-    const int t = e >> 3, c = e & 7;
-    const bool ok = t0 + t < T && c < k;
-    cp4(&S.Y[s][t][c], ok ? tg + (t0 + t) * k + c : tg, ok);
+  if (k == KX && ((reinterpret_cast<uintptr_t>(tg) & 15) == 0)) {
+    // 8 targets per row = two 16-byte pieces, 16 pieces per tile
+    if (lane < 2 * TT) {
+      const int t = lane >> 1, c4 = (lane & 1) * 4;
+      const bool ok = t0 + t < T;
+      cp16(&S.Y[s][t][c4], ok ? tg + (t0 + t) * KX + c4 : tg, ok);
+    }
+  } else {
+    for (int e = lane; e < TT * KX; e += 32) {
+      const int t = e >> 3, c = e & 7;
+      const bool ok = t0 + t < T && c < k;
+      cp4(&S.Y[s][t][c], ok ? tg + (t0 + t) * k + c : tg, ok);
+    }
   }
   asm volatile("cp.async.commit_group;\n" ::);
 }
@@ -287,7 +322,16 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
           // ---- dependent rows [rs, te): blocked Sherman-Morrison in LDL^T form -------
           const bool full_fold = r > 0;
           if (full_fold) {
-            // U = G P (t x i): lane (i = pi, t = 4 ph .. 4 ph + 3) -> U^T[i][t]
+            // U = G P (t x i): lane (i = pi, t = 4 ph .. 4 ph + 3); P's row pi read once
+            float pr[R];
+#pragma unroll
+            for (int l4 = 0; l4 < R; l4 += 4) {
+              const float4 pq = *reinterpret_cast<const float4*>(&S.P[pi][l4]);
+              pr[l4] = pq.x;
+              pr[l4 + 1] = pq.y;
+              pr[l4 + 2] = pq.z;
+              pr[l4 + 3] = pq.w;
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int t = 4 * ph + u;
@@ -295,19 +339,29 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
 #pragma unroll
               for (int l4 = 0; l4 < R; l4 += 4) {
                 const float4 gq = *reinterpret_cast<const float4*>(&S.G[t][l4]);
-                const float4 pq = *reinterpret_cast<const float4*>(&S.P[pi][l4]);
-                acc = fmaf(gq.x, pq.x, acc);
-                acc = fmaf(gq.y, pq.y, acc);
-                acc = fmaf(gq.z, pq.z, acc);
-                acc = fmaf(gq.w, pq.w, acc);
+                acc = fmaf(gq.x, pr[l4], acc);
+                acc = fmaf(gq.y, pr[l4 + 1], acc);
+                acc = fmaf(gq.z, pr[l4 + 2], acc);
+                acc = fmaf(gq.w, pr[l4 + 3], acc);
               }
               S.Us[t][pi] = (t >= rs && t < te) ? acc : 0.f;  // rows outside the run drop out
             }
           }
-          // M = I + U G^T (masked) and dy0 = y - a.x0 - G W: lane (t = l / 4, t'|c = 2 (l % 4) + e)
+          __syncwarp();
+          // M = I + U G^T (masked, in registers: lane (t = l / 4, t' = 2 (l % 4) + e)),
+          // dy0 = y - a.x0 - G W (same lanes, c = t'), then M = L D L^T by shuffles
           {
             const int t = lane >> 2, q2 = 2 * (lane & 3);
             const bool in_t = t >= rs && t < te;
+            float ur[R], gr[R];
+#pragma unroll
+            for (int i4 = 0; i4 < R; i4 += 4) {
+              const float4 u = *reinterpret_cast<const float4*>(&S.Us[t][i4]);
+              const float4 g1 = *reinterpret_cast<const float4*>(&S.G[t][i4]);
+              ur[i4] = u.x; ur[i4 + 1] = u.y; ur[i4 + 2] = u.z; ur[i4 + 3] = u.w;
+              gr[i4] = g1.x; gr[i4 + 1] = g1.y; gr[i4 + 2] = g1.z; gr[i4 + 3] = g1.w;
+            }
+            float mi[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int t2 = q2 + e;
@@ -315,76 +369,72 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
               if (full_fold) {
 #pragma unroll
                 for (int i4 = 0; i4 < R; i4 += 4) {
-                  const float4 u = *reinterpret_cast<const float4*>(&S.Us[t][i4]);
                   const float4 g2 = *reinterpret_cast<const float4*>(&S.G[t2][i4]);
-                  const float4 g1 = *reinterpret_cast<const float4*>(&S.G[t][i4]);
                   const float4 w = *reinterpret_cast<const float4*>(&S.Wt[t2][i4]);
-                  sv = fmaf(u.x, g2.x, sv);
-                  gwv = fmaf(g1.x, w.x, gwv);
-                  sv = fmaf(u.y, g2.y, sv);
-                  gwv = fmaf(g1.y, w.y, gwv);
-                  sv = fmaf(u.z, g2.z, sv);
-                  gwv = fmaf(g1.z, w.z, gwv);
-                  sv = fmaf(u.w, g2.w, sv);
-                  gwv = fmaf(g1.w, w.w, gwv);
+                  sv = fmaf(ur[i4], g2.x, sv);
+                  gwv = fmaf(gr[i4], w.x, gwv);
+                  sv = fmaf(ur[i4 + 1], g2.y, sv);
+                  gwv = fmaf(gr[i4 + 1], w.y, gwv);
+                  sv = fmaf(ur[i4 + 2], g2.z, sv);
+                  gwv = fmaf(gr[i4 + 2], w.z, gwv);
+                  sv = fmaf(ur[i4 + 3], g2.w, sv);
+                  gwv = fmaf(gr[i4 + 3], w.w, gwv);
                 }
               }
               const bool in2 = t2 >= rs && t2 < te;
-              S.Mm[t][t2] = (in_t && in2 ? sv : 0.f) + (t == t2 ? 1.f : 0.f);
-              S.Em[t][t2] = t == t2 ? 1.f : 0.f;
+              mi[e] = (in_t && in2 ? sv : 0.f) + (t == t2 ? 1.f : 0.f);
               S.Dy[t][t2] = in_t && t2 < k ? (S.Y[s][t][t2] - S.G[t][16 + t2]) - gwv : 0.f;
+            }
+            if (full_fold) {
+              float ev[2], rd0, rd1;
+              ldl8f(mi, ev, rd0, rd1, t, lane & 3);
+              S.Em[t][q2] = ev[0];
+              S.Em[t][q2 + 1] = ev[1];
+              if (t == 0) {
+                S.rd[q2] = rd0;
+                S.rd[q2 + 1] = rd1;
+              }
             }
           }
           __syncwarp();
           if (full_fold) {
-            // M = L D L^T by elimination, E = L^-1 (lane: row t = l / 4, columns 2 (l % 4) + e)
             const int t = lane >> 2, q2 = 2 * (lane & 3);
-            float mv[2] = {S.Mm[t][q2], S.Mm[t][q2 + 1]};
-            float ev[2] = {S.Em[t][q2], S.Em[t][q2 + 1]};
+            // Y = U^T E^T (i x t): lane (i = pi, t = 4 ph + u); U's column pi read once
+            float uc[TT];
 #pragma unroll
-            for (int kk = 0; kk < TT - 1; ++kk) {
-              const float rpiv = rcpf(S.Mm[kk][kk]);
-              const float f = t > kk ? S.Mm[t][kk] * rpiv : 0.f;
-              const float mk0 = S.Mm[kk][q2], mk1 = S.Mm[kk][q2 + 1];
-              const float ek0 = S.Em[kk][q2], ek1 = S.Em[kk][q2 + 1];
-              mv[0] = fmaf(-f, mk0, mv[0]);
-              mv[1] = fmaf(-f, mk1, mv[1]);
-              ev[0] = fmaf(-f, ek0, ev[0]);
-              ev[1] = fmaf(-f, ek1, ev[1]);
-              __syncwarp();
-              S.Mm[t][q2] = mv[0];
-              S.Mm[t][q2 + 1] = mv[1];
-              S.Em[t][q2] = ev[0];
-              S.Em[t][q2 + 1] = ev[1];
-              __syncwarp();
-            }
-            if (lane < TT) S.rd[lane] = rcpf(S.Mm[lane][lane]);
-            __syncwarp();
-            // Y = U^T E^T (i x t): lane (i = pi, t = 4 ph + u)
+            for (int t2 = 0; t2 < TT; ++t2) uc[t2] = S.Us[t2][pi];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int tt = 4 * ph + u;
               const float4 e0 = *reinterpret_cast<const float4*>(&S.Em[tt][0]);
               const float4 e1 = *reinterpret_cast<const float4*>(&S.Em[tt][4]);
-              float acc = S.Us[0][pi] * e0.x;
-              acc = fmaf(S.Us[1][pi], e0.y, acc);
-              acc = fmaf(S.Us[2][pi], e0.z, acc);
-              acc = fmaf(S.Us[3][pi], e0.w, acc);
-              acc = fmaf(S.Us[4][pi], e1.x, acc);
-              acc = fmaf(S.Us[5][pi], e1.y, acc);
-              acc = fmaf(S.Us[6][pi], e1.z, acc);
-              acc = fmaf(S.Us[7][pi], e1.w, acc);
+              float acc = uc[0] * e0.x;
+              acc = fmaf(uc[1], e0.y, acc);
+              acc = fmaf(uc[2], e0.z, acc);
+              acc = fmaf(uc[3], e0.w, acc);
+              acc = fmaf(uc[4], e1.x, acc);
+              acc = fmaf(uc[5], e1.y, acc);
+              acc = fmaf(uc[6], e1.z, acc);
+              acc = fmaf(uc[7], e1.w, acc);
               S.Yy[pi][tt] = acc;
             }
-            // dh = D^-1 E dy0 (t x c): lane (t = l / 4, c = 2 (l % 4) + e)
+            // dh = D^-1 E dy0 (t x c): lane (t = l / 4, c = 2 (l % 4) + e); E's row t read once
+            float er[TT];
+            {
+              const float4 e0 = *reinterpret_cast<const float4*>(&S.Em[t][0]);
+              const float4 e1 = *reinterpret_cast<const float4*>(&S.Em[t][4]);
+              er[0] = e0.x; er[1] = e0.y; er[2] = e0.z; er[3] = e0.w;
+              er[4] = e1.x; er[5] = e1.y; er[6] = e1.z; er[7] = e1.w;
+            }
+            const float rdt = S.rd[t];
             float dh[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int c = q2 + e;
               float acc = 0.f;
 #pragma unroll
-              for (int t2 = 0; t2 < TT; ++t2) acc = fmaf(S.Em[t][t2], S.Dy[t2][c], acc);
-              dh[e] = acc * S.rd[t];
+              for (int t2 = 0; t2 < TT; ++t2) acc = fmaf(er[t2], S.Dy[t2][c], acc);
+              dh[e] = acc * rdt;
             }
             S.DhT[q2][t] = dh[0];
             S.DhT[q2 + 1][t] = dh[1];
