@@ -96,7 +96,8 @@ struct Ws {  // global workspace layout (doubles), per launch
   __host__ __device__ static size_t gpart(int nc) { return (size_t)nc * TT * GX; }
   static size_t bytes(int nc) {
     return 256 + sizeof(double) * (gpart(nc) + TT * GX + (size_t)nc * 4 * TT + (size_t)(R / 8) * 2 * 64 +
-                                   (size_t)R * TT + (size_t)R * 8 + (size_t)R + (size_t)(R / 8) * 16);
+                                   (size_t)R * TT + (size_t)R * 8 + (size_t)R + (size_t)(R / 8) * 16 +
+                                   (size_t)nc * 64);
   }
 };
 
@@ -141,9 +142,11 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
   double* ws_w = ws_y + (size_t)R * TT;            // [R][8]
   double* ws_z = ws_w + (size_t)R * 8;             // [R]: z = P gamma (non-general growth)
   double* ws_d = ws_z + R;                         // [IT][16]: gamma.z, gamma^T W partials
+  double* ws_m = ws_d + (size_t)IT * 16;           // [nc][64]: R R^T partials (block growth)
   unsigned epoch = 0;
 #ifdef RGB_GRID_PROBE
   unsigned long long probe_t = ggtime();
+  const unsigned long long probe_t0 = probe_t;
 #endif
   unsigned nproj = 0;  // projections so far (selects the ws_r buffer)
 
@@ -186,6 +189,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       pending_p6 = false;
     };
     const int64_t nobs0 = st.nobs[b];
+    // certified block growth of a fresh stream's leading rows (general variant,
+    // x0 = 0): on until the first tile with a row it cannot certify
+    bool bulk = (GEN || cfg.variant == RGB_GENERAL) && r == 0 && nobs0 == 0;
     double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)rc * M;
     double* Dg = reinterpret_cast<double*>(st.dual) + b * (int64_t)rc * M;
     double* Pg = reinterpret_cast<double*>(st.gram_inv) + b * (int64_t)rc * rc;
@@ -224,6 +230,10 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
       const int64_t t0 = tile * TT;
       const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
+#ifdef RGB_GRID_PROBE
+      // elapsed time until the stream's rank first reaches its final value's tile
+      if (threadIdx.x == 0 && blockIdx.x < 2 && tile == (int64_t)(R / 8)) g_gprobe[blockIdx.x][12] = ggtime() - probe_t0;
+#endif
       // tile rows of my columns and the targets
       for (int e = tid; e < TT * CW; e += NT) {
         const int t = e / CW, j = e % CW;
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         // a tile whose rows are all independent runs no barrier between the
         // test's reads of ws_r and the next projection's writes: alternate buffers
         double* ws_r = ws_r0 + (size_t)(nproj++ & 1u) * nc * 2 * TT;
+        const bool bulk_try = bulk && row_start == 0 && tv == TT && r + TT <= rc;
         // ---- P1: G partial of my columns (M = t, N = i, K = my columns) -> ws
         // (N tiles past the rank are zero: skipped here, zeroed by the reducers)
         const int nlive = (r + 7) >> 3;
@@ -365,6 +376,16 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             for (int j = 0; j < CW; ++j) s = fma(S.Rs[tid][j], S.Rs[tid][j], s);
             ws_r[((size_t)0 * TT + tid) * nc + c] = s;
           }
+          if (bulk_try && w == 1) {
+            // R R^T over my columns (M = t, N = t', K = j): the same fragment is both operands
+            double acc[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kt = 0; kt < CW / 4; ++kt) {
+              const double v = S.Rs[p][4 * kt + q];
+              mma(acc, v, v);
+            }
+            *reinterpret_cast<double2*>(ws_m + (size_t)c * 64 + p * 8 + 2 * q) = make_double2(acc[0], acc[1]);
+          }
         }
         // U_b = P_b G^T and the S / G W partials of every row of the tile, before the
         // rank test is known: the rows the test leaves out are masked afterwards
@@ -427,6 +448,135 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
         }
         __syncthreads();
+        if (bulk_try) {
+          // ---- certified block growth (general variant, x0 = 0; the panel kernel's
+          // algebra, rgb_panel.cu): for a tile of independent rows the reference's
+          // row-by-row growth (solver.py:305-318, _grow :368-380) is one block step
+          // -- Z = (R R^T)^-1 R are the new dual rows, C~ - G^T Z the old ones, C
+          // gains the rows, P^-1 = diag(P^-1, I), W gains y.  The pivot d_t of
+          // R R^T = L D L^T is row t's squared rejection from the basis plus the
+          // tile's rows before it; a row is certified when d_t clears the rank test
+          // by BULK_MARGIN and keeps >= BULK_COND of |R_t|^2.  The certified prefix
+          // is grown here (3 grid barriers per 8 rows instead of per row); the
+          // first uncertified row ends the bulk phase and goes to the exact test.
+          constexpr double BULK_COND = 0.1, BULK_MARGIN = 1e6;
+          {
+            // R R^T = the CTAs' partials summed in a fixed order (identical in every CTA)
+            const int e = tid & 63, g = tid >> 6;
+            constexpr int PER = (148 + NT / 64 - 1) / (NT / 64);
+            double v[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+              const int u = g + (NT / 64) * i;
+              v[i] = u < nc ? __ldcg(ws_m + (size_t)u * 64 + e) : 0.0;
+            }
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) sum += v[i];
+            S.red[4 + g][e] = sum;
+          }
+          __syncthreads();
+          if (w == 0) {
+            double mm[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int idx = p * 8 + 2 * q + e;
+              mm[e] = ((S.red[4][idx] + S.red[5][idx]) + S.red[6][idx]) + S.red[7][idx];
+            }
+            // a non-finite row enters as the identity (0 x NaN in the elimination
+            // would reach the earlier rows); it fails the certification anyway
+            double mi[2], ev[2], rd0, rd1;
+            {
+              const bool badp = !isfinite(S.red[0][TT + p]);
+              const bool badc0 = !isfinite(S.red[0][TT + 2 * q]);
+              const bool badc1 = !isfinite(S.red[0][TT + 2 * q + 1]);
+              mi[0] = (badp || badc0) ? (p == 2 * q ? 1.0 : 0.0) : mm[0];
+              mi[1] = (badp || badc1) ? (p == 2 * q + 1 ? 1.0 : 0.0) : mm[1];
+            }
+            blk::ldl8(mi, ev, rd0, rd1, p, q);
+            const int t = lane & 7;
+            const double x0 = __shfl_sync(FULL, rd0, t >> 1), x1 = __shfl_sync(FULL, rd1, t >> 1);
+            const double rdt = (t & 1) ? x1 : x0;
+            const double y0 = __shfl_sync(FULL, mm[0], 4 * t + (t >> 1));
+            const double y1 = __shfl_sync(FULL, mm[1], 4 * t + (t >> 1));
+            const double mtt = (t & 1) ? y1 : y0;
+            const double at = S.red[0][TT + t];
+            bool yok = true;
+            for (int cc = 0; cc < k; ++cc) yok &= isfinite(S.Yv[t][cc]);
+            const double dt = 1.0 / rdt;
+            const double e2 = eps_sq<double>(cfg, r + t);
+            const bool ok = isfinite(at) && yok && dt > BULK_COND * mtt && dt > BULK_MARGIN * e2 * fmax(1.0, at);
+            const unsigned failm = __ballot_sync(FULL, lane < TT && !ok);
+            const int tst = failm ? __ffs(failm) - 1 : TT;
+            S.Eb[p][2 * q] = ev[0];
+            S.Eb[p][2 * q + 1] = ev[1];
+            if (lane < TT) S.rd[lane] = rdt;
+            if (lane == 0) S.flags[2] = tst;
+          }
+          __syncthreads();
+          const int tst = S.flags[2];
+          if (tst < TT) bulk = false;
+          if (tst > 0) {
+            // Q = D^-1 E R, then Z = E^T Q on my columns (rows t < tst)
+            double* Qs = &S.red[1][0];
+            double* Zs = &S.red[2][0];
+            for (int e = tid; e < TT * CW; e += NT) {
+              const int t = e / CW, j = e % CW;
+              double v = 0.0;
+              for (int t2 = 0; t2 <= t && t2 < tst; ++t2) v = fma(S.Eb[t][t2], S.Rs[t2][j], v);
+              Qs[e] = t < tst ? v * S.rd[t] : 0.0;
+            }
+            __syncthreads();
+            for (int e = tid; e < TT * CW; e += NT) {
+              const int t = e / CW, j = e % CW;
+              double v = 0.0;
+              for (int t2 = tst - 1; t2 >= t; --t2) v = fma(S.Eb[t2][t], Qs[t2 * CW + j], v);
+              Zs[e] = t < tst ? v : 0.0;
+            }
+            __syncthreads();
+            // C~[:r] -= G^T Z, C~[r + t] = Z[t] on my columns; C[r + t] = a_t
+            for (int e = tid; e < IT * (CW / 4) * 32; e += NT) {
+              const int l = e & 31, kt = (e >> 5) % (CW / 4), nt = e / (32 * (CW / 4));
+              const int i = 8 * nt + (l >> 2), jl = 4 * kt + (l & 3);
+              if (i < r) {
+                double v = S.Ds[nt][kt][l];
+                for (int t = 0; t < tst; ++t) v -= S.Gs[t][i] * Zs[t * CW + jl];
+                S.Ds[nt][kt][l] = v;
+              } else if (i < r + tst) {
+                S.Ds[nt][kt][l] = Zs[(i - r) * CW + jl];
+              }
+            }
+            for (int e = tid; e < tst * CW; e += NT) {
+              const int t = e / CW, jl = e % CW, i = r + t;
+              S.Cs[i >> 2][jl >> 3][4 * (jl & 7) + (i & 3)] = -S.At[t][jl];
+            }
+            if (owner) {
+              // P = diag(P, I); W gains rows y_t - a_t.x0 (a.x0 = 0 here)
+              for (int e = tid; e < 8 * R; e += NT) {
+                const int i = 8 * c + e / R, i2 = e % R;
+                const bool ni = i >= r && i < r + tst, ni2 = i2 >= r && i2 < r + tst;
+                if (ni || ni2) S.Ps[e / R][i2] = (i == i2) ? 1.0 : 0.0;
+              }
+              if (tid < 64) {
+                const int i = 8 * c + (tid >> 3), cc = tid & 7;
+                if (i >= r && i < r + tst) S.Wb[tid >> 3][cc] = cc < k ? S.Yv[i - r][cc] - S.Gs[i - r][R + cc] : 0.0;
+              }
+            }
+            if (c == 0) {
+              for (int t = tid; t < tst; t += NT)
+                if (blog) blog[b * T + t0 + t] = 1;
+              if (clog)
+                for (int e = tid; e < tst * rc; e += NT)
+                  clog[(b * T + t0 + e / rc) * rc + e % rc] = (e % rc == r + e / rc) ? 1.0 : 0.0;
+            }
+            __syncthreads();
+            r += tst;
+            if (tst >= tv) break;    // the whole tile grew
+            row_start = tst;         // the rest of the tile: re-projected on the new basis
+            continue;
+          }
+          // nothing certified: the exact rank test below, on this projection
+        }
         if (w == 0) {
           const double rsq = lane < TT ? S.red[0][lane] : 0.0;
           const double asq = lane < TT ? S.red[0][TT + lane] : 0.0;

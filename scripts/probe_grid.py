@@ -30,7 +30,8 @@ for i in range(2):
     e1.record()
     torch.cuda.synchronize()
 lib.rgb_grid_probe(buf.ctypes.data, 0)
-names = ["P6+grow+P1", "bar1", "P2 reduce", "bar2", "P3", "bar3", "P4+U/S", "bar4", "P5 LDL/Y", "bar5", "grow-ng", "bar-ng"]
+names = ["P6+grow+P1", "bar1", "P2 reduce", "bar2", "P3", "bar3", "P4+U/S", "bar4", "P5 LDL/Y", "bar5", "grow-ng", "bar-ng",
+         "t(first R rows)"]
 print(cfg, "kernel ms", e0.elapsed_time(e1))
 for k in range(2):
     print("CTA", k, {n: round(buf[k][i] / 1e6, 3) for i, n in enumerate(names)})
