@@ -227,6 +227,22 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
     const int64_t ntiles = (T + TT - 1) / TT;
     int64_t consumed = 0;
     bool stopped = false;
+    // the next tile's rows of my columns and its targets are loaded into registers
+    // one tile ahead (their HBM latency overlaps the current tile's phases)
+    constexpr int PA = (TT * CW + NT - 1) / NT;
+    double na[PA], ny = 0.0;
+    auto load_next = [&](int64_t tile) {
+      const int64_t t0 = tile * TT;
+#pragma unroll
+      for (int i = 0; i < PA; ++i) {
+        const int e = tid + NT * i, t = e / CW, j = e % CW;
+        na[i] = (e < TT * CW && tile < ntiles && t0 + t < T && c0 + j < M) ? (double)__ldg(Rb + (t0 + t) * M + c0 + j)
+                                                                         : 0.0;
+      }
+      const int t = tid >> 3, cc = tid & 7;
+      ny = (tid < 64 && tile < ntiles && t0 + t < T && cc < k) ? (double)__ldg(Yb + (t0 + t) * k + cc) : 0.0;
+    };
+    load_next(0);
     for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
       const int64_t t0 = tile * TT;
       const int tv = (int)((T - t0) < TT ? (T - t0) : TT);
@@ -234,15 +250,14 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       // elapsed time until the stream's rank first reaches its final value's tile
       if (threadIdx.x == 0 && blockIdx.x < 2 && tile == (int64_t)(R / 8)) g_gprobe[blockIdx.x][12] = ggtime() - probe_t0;
 #endif
-      // tile rows of my columns and the targets
-      for (int e = tid; e < TT * CW; e += NT) {
-        const int t = e / CW, j = e % CW;
-        S.At[t][j] = (t < tv && c0 + j < M) ? (double)Rb[(t0 + t) * M + c0 + j] : 0.0;
+      // tile rows of my columns and the targets (loaded one tile ahead)
+#pragma unroll
+      for (int i = 0; i < PA; ++i) {
+        const int e = tid + NT * i;
+        if (e < TT * CW) S.At[e / CW][e % CW] = na[i];
       }
-      for (int e = tid; e < 64; e += NT) {
-        const int t = e >> 3, cc = e & 7;
-        S.Yv[t][cc] = (t < tv && cc < k) ? (double)Yb[(t0 + t) * k + cc] : 0.0;
-      }
+      if (tid < 64) S.Yv[tid >> 3][tid & 7] = ny;
+      load_next(tile + 1);
       __syncthreads();
       int row_start = 0;
       while (true) {
@@ -291,26 +306,34 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           const int chunk = (NE + nc - 1) / nc;
           const int e0 = c * chunk, e1 = (e0 + chunk < NE) ? e0 + chunk : NE;
           constexpr int MAXU = (148 + NW - 1) / NW;  // partials per warp (one CTA per SM)
-          for (int eb = e0; eb < e1; eb += 32) {
-            const int e = eb + lane;
-            const int col = e % GX;  // G column: coordinate i < R, or R + c for a.x0
-            const bool live = e < e1 && (col >= R || col < 8 * nlive);
-            double v[MAXU];  // every load in flight before the (fixed-order) sum
+          // two elements per lane per round: a chunk of up to 64 elements (nc >= 66) is
+          // one round of loads, all in flight before the (fixed-order) sums
+          for (int eb = e0; eb < e1; eb += 64) {
+            double v[2][MAXU];
 #pragma unroll
-            for (int i = 0; i < MAXU; ++i) {
-              const int u = w + NW * i;
-              v[i] = (live && u < nc) ? __ldcg(ws_g + (size_t)u * NE + e) : 0.0;
+            for (int h = 0; h < 2; ++h) {
+              const int e = eb + 32 * h + lane;
+              const int col = e % GX;  // G column: coordinate i < R, or R + c for a.x0
+              const bool live = e < e1 && (col >= R || col < 8 * nlive);
+#pragma unroll
+              for (int i = 0; i < MAXU; ++i) {
+                const int u = w + NW * i;
+                v[h][i] = (live && u < nc) ? __ldcg(ws_g + (size_t)u * NE + e) : 0.0;
+              }
             }
-            double sum = 0.0;
 #pragma unroll
-            for (int i = 0; i < MAXU; ++i) sum += v[i];
-            S.red[w][lane] = sum;
+            for (int h = 0; h < 2; ++h) {
+              double sum = 0.0;
+#pragma unroll
+              for (int i = 0; i < MAXU; ++i) sum += v[h][i];
+              S.red[w][32 * h + lane] = sum;
+            }
             __syncthreads();
-            if (w == 0 && e < e1) {
+            if (w < 2 && eb + 32 * w + lane < e1) {
               double v = 0.0;
 #pragma unroll
-              for (int u = 0; u < NW; ++u) v += S.red[u][lane];
-              ws_gf[e] = v;
+              for (int u = 0; u < NW; ++u) v += S.red[u][32 * w + lane];
+              ws_gf[eb + 32 * w + lane] = v;
             }
             __syncthreads();
           }
@@ -424,7 +447,20 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
         grid_sync(ctr, epoch);
         GPROBE(5);
         // ---- P4: the rank test (identical in every CTA).  Warp t sums row t's
-        // partials (lane l: CTAs l, l+32, ...; then a fixed butterfly).
+        // partials (lane l: CTAs l, l+32, ...; then a fixed butterfly).  The owners'
+        // S and G W partials are loaded in the same round (used if rows are dependent).
+        constexpr int SPER = (IT + NW - 1) / NW;
+        double2 s2[SPER], g2[SPER];
+        if (owner) {
+#pragma unroll
+          for (int i = 0; i < SPER; ++i) {
+            const int u = w + NW * i;
+            s2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q))
+                           : make_double2(0.0, 0.0);
+            g2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q))
+                           : make_double2(0.0, 0.0);
+          }
+        }
         {
           constexpr int PER = (148 + 31) / 32;  // one CTA per SM
           double rv[PER], av[PER];
@@ -603,19 +639,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           if (owner) {
             {
               // sums of the S and G W partials: warp w takes owners w, w+8, ...
-              double a4[4] = {0.0, 0.0, 0.0, 0.0};
-              constexpr int PER = (IT + NW - 1) / NW;
-              double2 s2[PER], g2[PER];  // all in flight, then summed in owner order
+              double a4[4] = {0.0, 0.0, 0.0, 0.0};  // loaded with the rank test, summed in owner order
 #pragma unroll
-              for (int i = 0; i < PER; ++i) {
-                const int u = w + NW * i;
-                s2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2) * 64 + p * 8 + 2 * q))
-                               : make_double2(0.0, 0.0);
-                g2[i] = u < IT ? __ldcg(reinterpret_cast<const double2*>(ws_s + ((size_t)u * 2 + 1) * 64 + p * 8 + 2 * q))
-                               : make_double2(0.0, 0.0);
-              }
-#pragma unroll
-              for (int i = 0; i < PER; ++i) {
+              for (int i = 0; i < SPER; ++i) {
                 a4[0] += s2[i].x;
                 a4[1] += s2[i].y;
                 a4[2] += g2[i].x;
