@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define RGB_ABI_VERSION 3
+#define RGB_ABI_VERSION 4
 
 /* scalar kinds: scalars.py:141-147 (FLOAT64); FLOAT32 is a new kind */
 enum { RGB_F64 = 0, RGB_F32 = 1 };
@@ -170,6 +170,8 @@ int rgb_covariance(const rgb_config *cfg, const rgb_state *state, void *out, voi
 #define RGB_ROWPIPE_OFF_RANK 16
 #define RGB_ROWPIPE_OFF_STATUS 20
 #define RGB_ROWPIPE_OFF_BRANCH 24
+#define RGB_ROWPIPE_OFF_REQ 32  /* u64: row server request (the row number), written by rgb_rowpipe_run */
+#define RGB_ROWPIPE_OFF_STOP 40 /* u32: row server stop word, written by rgb_rowpipe_quiesce */
 typedef struct rgb_rowpipe rgb_rowpipe;
 
 /* Size of a row pipe's host block (bytes) and the offsets of its areas. */
@@ -182,8 +184,18 @@ int64_t rgb_rowpipe_layout(const rgb_config *cfg, int f32in, int64_t *off_in, in
  * live `solution` view (solver.py:200-202). */
 int rgb_rowpipe_create(const rgb_config *cfg, const rgb_state *state, int want_report, int f32in,
                        void *host_x, rgb_rowpipe **pipe, void **host_block);
-/* Fold the row staged in the block; blocks until its report is visible. */
+/* Fold the row staged in the block; blocks until its report is visible.
+ * Where the one-row kernel applies (the state fits its shared memory) the row
+ * goes to a ROW SERVER: a one-CTA persistent kernel on the pipe's own stream
+ * that keeps the state in shared memory, polls the block for requests and
+ * exits after RGB_ROWSERVE_IDLE_US microseconds without one (environment, read
+ * at create; default 500, 0 = one graph launch per row).  It is launched on
+ * demand, ordered after the work already on `stream`. */
 int rgb_rowpipe_run(rgb_rowpipe *pipe, void *stream);
+/* Stop the pipe's row server (if it runs) and wait for it: call before any
+ * other kernel writes the state (an ingest of several rows, a reset).
+ * rgb_rowpipe_destroy stops it too. */
+int rgb_rowpipe_quiesce(rgb_rowpipe *pipe);
 void rgb_rowpipe_destroy(rgb_rowpipe *pipe);
 
 #ifdef __cplusplus

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # RGB_LIB_PATH selects an alternative build of the same library (tuning A/B runs)
 LIB_PATH = os.environ.get("RGB_LIB_PATH") or os.path.join(HERE, "librgb.so")
 
-RGB_ABI_VERSION = 3
+RGB_ABI_VERSION = 4
 F64, F32 = 0, 1
 GENERAL, ORTHOGONAL, ORTHONORMAL = 0, 1, 2
 EPS_AUTO, EPS_FIXED = 0, 1
@@ -24,10 +24,11 @@ ST_RANK_CAP, ST_NONFINITE, ST_BAD_ALPHA = 1, 2, 4
 EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest", "rgb_ingest_f32in",
            "rgb_memcpy_async",
            "rgb_project", "rgb_pinv", "rgb_covariance",
-           "rgb_rowpipe_layout", "rgb_rowpipe_create", "rgb_rowpipe_run", "rgb_rowpipe_destroy")
+           "rgb_rowpipe_layout", "rgb_rowpipe_create", "rgb_rowpipe_run", "rgb_rowpipe_quiesce",
+           "rgb_rowpipe_destroy")
 # row pipe host-block header (include/rgb.h)
 ROWPIPE_HEADER, ROWPIPE_OFF_SEQ, ROWPIPE_OFF_NOBS, ROWPIPE_OFF_RANK = 64, 0, 8, 16
-ROWPIPE_OFF_STATUS, ROWPIPE_OFF_BRANCH = 20, 24
+ROWPIPE_OFF_STATUS, ROWPIPE_OFF_BRANCH, ROWPIPE_OFF_REQ, ROWPIPE_OFF_STOP = 20, 24, 32, 40
 
 
 class Config(ctypes.Structure):
@@ -98,6 +99,7 @@ def load():
     lib.rgb_rowpipe_create.argtypes = [cfgp, stp, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp),
                                        ctypes.POINTER(vp)]
     lib.rgb_rowpipe_run.argtypes = [vp, vp]
+    lib.rgb_rowpipe_quiesce.argtypes = [vp]
     lib.rgb_rowpipe_destroy.argtypes = [vp]
     for name in EXPORTS[2:]:
         getattr(lib, name).restype = ctypes.c_int

@@ -57,50 +57,58 @@ __device__ __forceinline__ void r1_publish(unsigned char* mirror, unsigned long 
 // (Measured alternative: a plain launch carrying the row in a 3 KB kernel
 // parameter instead of the graph plus the host-memory read: 17.5 vs 14.6 us
 // per call at m = 128.)
+// shared-memory layout of the row kernels: the row and its scratch, then the state
 template <typename REAL>
-__global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state st, const REAL* __restrict__ a_g,
-                                                     const REAL* __restrict__ y_g, rgb_logs logs,
-                                                     unsigned char* __restrict__ mirror,
-                                                     unsigned long long* __restrict__ dseq, REAL* __restrict__ hx) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
-  const bool onorm = var == RGB_ORTHONORMAL;
-  REAL* a_s = reinterpret_cast<REAL*>(smem_raw);
-  REAL* rej_s = a_s + m;
-  REAL* gam = rej_s + m;
-  REAL* z_s = gam + rc;
-  REAL* y_s = z_s + rc;
-  REAL* red = y_s + R1_MK;                     // [NW][MK + 2]
-  REAL* Cg = reinterpret_cast<REAL*>(st.basis);
-  REAL* Dg = onorm ? Cg : reinterpret_cast<REAL*>(st.dual);
-  REAL* D = red + R1_NW * (R1_MK + 2);         // C~ rows < r
-  REAL* C = onorm ? D : D + (size_t)rc * m;    // C rows < r
-  REAL* P = C + (size_t)rc * m;                // P^-1 [r][r] at stride rc
-  REAL* X = P + (size_t)rc * rc;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv);
-  REAL* Xg = reinterpret_cast<REAL*>(st.x);
-  int r = st.rank[0];
-  int status = st.status[0];
-  int64_t nobs = st.nobs[0];
-  if (status) {
-    r1_publish<REAL>(mirror, dseq, nobs, r, status, tid);
-    return;
+struct R1Smem {
+  REAL *a_s, *rej_s, *gam, *z_s, *y_s, *red, *zd, *dyv, *D, *C, *P, *X;
+  __device__ R1Smem(unsigned char* raw, const rgb_config& cfg) {
+    const int m = cfg.m, rc = cfg.r_cap;
+    a_s = reinterpret_cast<REAL*>(raw);
+    rej_s = a_s + m;
+    gam = rej_s + m;
+    z_s = gam + rc;
+    y_s = z_s + rc;
+    red = y_s + R1_MK;                                       // [NW][MK + 2]
+    zd = red + R1_NW * (R1_MK + 2);                          // z / denom
+    dyv = zd + rc;                                           // y - a.x (a-priori residuals)
+    D = dyv + R1_MK;                                         // C~ rows < r
+    C = cfg.variant == RGB_ORTHONORMAL ? D : D + (size_t)rc * m;  // C rows < r
+    P = C + (size_t)rc * m;                                  // P^-1 [r][r] at stride rc
+    X = P + (size_t)rc * rc;
   }
-  // ---- stage: the row and targets (host memory) first, then the state ------------
-  for (int j = tid; j < m; j += R1_NT) r1_cp(a_s + j, a_g + j, sizeof(REAL));
-  for (int c = tid; c < k; c += R1_NT) r1_cp(y_s + c, y_g + c, sizeof(REAL));
-  for (int e = tid; e < r * m; e += R1_NT) r1_cp(D + e, Dg + e, sizeof(REAL));
-  if (!onorm)
-    for (int e = tid; e < r * m; e += R1_NT) r1_cp(C + e, Cg + e, sizeof(REAL));
+};
+
+// the state into shared memory (cp.async; the caller commits and waits)
+template <typename REAL>
+__device__ __forceinline__ void r1_stage_state(const rgb_config& cfg, const REAL* Cg, const REAL* Dg, const REAL* Pg,
+                                               const REAL* Xg, const R1Smem<REAL>& S_, int r) {
+  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, tid = threadIdx.x;
+  for (int e = tid; e < r * m; e += R1_NT) r1_cp(S_.D + e, Dg + e, sizeof(REAL));
+  if (cfg.variant != RGB_ORTHONORMAL)
+    for (int e = tid; e < r * m; e += R1_NT) r1_cp(S_.C + e, Cg + e, sizeof(REAL));
   for (int e = tid; e < r * r; e += R1_NT) {
     const int i = e / r, l = e - i * r;
-    r1_cp(P + (size_t)i * rc + l, Pg + (size_t)i * rc + l, sizeof(REAL));
+    r1_cp(S_.P + (size_t)i * rc + l, Pg + (size_t)i * rc + l, sizeof(REAL));
   }
-  for (int e = tid; e < k * m; e += R1_NT) r1_cp(X + e, Xg + e, sizeof(REAL));
-  asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
+  for (int e = tid; e < k * m; e += R1_NT) r1_cp(S_.X + e, Xg + e, sizeof(REAL));
+}
+
+// The fold of the staged row (a_s, y_s) on the staged state, phases A-D: results
+// straight to global memory (and, for the row server, SERVE, into the staged
+// state too, which it keeps between rows).  r, status, nobs are updated.
+template <typename REAL, bool SERVE>
+__device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state& st, const rgb_logs& logs,
+                                          const R1Smem<REAL>& S_, int& r, int& status, int64_t& nobs, REAL* hx) {
+  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
+  const bool onorm = var == RGB_ORTHONORMAL;
+  REAL *a_s = S_.a_s, *rej_s = S_.rej_s, *gam = S_.gam, *z_s = S_.z_s, *y_s = S_.y_s, *red = S_.red;
+  REAL *zd = S_.zd, *dyv = S_.dyv;
+  REAL *D = S_.D, *C = S_.C, *P = S_.P, *X = S_.X;
+  REAL* Cg = reinterpret_cast<REAL*>(st.basis);
+  REAL* Dg = onorm ? Cg : reinterpret_cast<REAL*>(st.dual);
+  REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv);
+  REAL* Xg = reinterpret_cast<REAL*>(st.x);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   // ---- A: coords (warp per dual row) and the |a|^2, a.x_c block partials ---------
   for (int i = w; i < r; i += R1_NW) {
     const REAL* d = D + (size_t)i * m;
@@ -171,8 +179,13 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
   if (bad) status |= RGB_ST_NONFINITE;
   else if (!dep && r >= rc) status |= RGB_ST_RANK_CAP;
   if (!status) {
-    // a-priori residual y_c - a.x_c (recomputed where used: same bits, no local array)
-    auto dy = [&](int c) { return y_s[c] - total(2 + c); };
+    // a-priori residuals y_c - a.x_c and z / denom, once (the same bits as forming
+    // them where used)
+    for (int c = tid; c < k; c += R1_NT) dyv[c] = y_s[c] - total(2 + c);
+    if (dep)
+      for (int i = tid; i < r; i += R1_NT) zd[i] = z_s[i] / denom;
+    __syncthreads();
+    auto dy = [&](int c) { return dyv[c]; };
     if (tid == 0 && logs.branch) logs.branch[0] = dep ? 0 : 1;
     if (logs.resid)
       for (int c = tid; c < k; c += R1_NT) reinterpret_cast<REAL*>(logs.resid)[c] = dy(c);
@@ -182,18 +195,20 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
       if (r > 0) {
         for (int idx = tid; idx < r * r; idx += R1_NT) {
           const int i = idx / r, l = idx - i * r;
-          const REAL zs = z_s[l] / denom;
+          const REAL zs = zd[l];
           REAL pv = P[(size_t)i * rc + l];
           pv -= z_s[i] * zs;
           Pg[(size_t)i * rc + l] = pv;
+          if constexpr (SERVE) P[(size_t)i * rc + l] = pv;
         }
         for (int j = tid; j < m; j += R1_NT) {
           REAL g = 0;
-          for (int i = 0; i < r; ++i) g = fma(z_s[i] / denom, D[(size_t)i * m + j], g);
+          for (int i = 0; i < r; ++i) g = fma(zd[i], D[(size_t)i * m + j], g);
           for (int c = 0; c < k; ++c) {
             REAL xv = X[(size_t)c * m + j];
             xv += g * dy(c);
             Xg[(size_t)c * m + j] = xv;
+            if constexpr (SERVE) X[(size_t)c * m + j] = xv;
             if (c == 0 && hx) hx[j] = xv;
           }
           if (gl) gl[j] = g;
@@ -209,17 +224,27 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
             REAL dv = D[(size_t)i * m + j];
             dv -= gam[i] * g;                        // solver.py:378
             Dg[(size_t)i * m + j] = dv;
+            if constexpr (SERVE) D[(size_t)i * m + j] = dv;
           }
           Dg[(size_t)r * m + j] = g;                 // solver.py:379
           Cg[(size_t)r * m + j] = a_s[j];            // solver.py:376
+          if constexpr (SERVE) {
+            D[(size_t)r * m + j] = g;
+            C[(size_t)r * m + j] = a_s[j];
+          }
         } else {
           Cg[(size_t)r * m + j] = alpha * rej_s[j];  // solver.py:384
           if (var == RGB_ORTHOGONAL) Dg[(size_t)r * m + j] = rej_s[j] / (alpha * rej_sq);
+          if constexpr (SERVE) {
+            C[(size_t)r * m + j] = alpha * rej_s[j];  // (orthonormal: D aliases C)
+            if (var == RGB_ORTHOGONAL) D[(size_t)r * m + j] = rej_s[j] / (alpha * rej_sq);
+          }
         }
         for (int c = 0; c < k; ++c) {
           REAL xv = X[(size_t)c * m + j];
           xv += g * dy(c);
           Xg[(size_t)c * m + j] = xv;
+          if constexpr (SERVE) X[(size_t)c * m + j] = xv;
           if (c == 0 && hx) hx[j] = xv;
         }
         if (gl) gl[j] = g;
@@ -233,14 +258,47 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
         if (i < r) {
           Pg[(size_t)i * rc + r] = edge;
           Pg[(size_t)r * rc + i] = edge;
+          if constexpr (SERVE) P[(size_t)i * rc + r] = P[(size_t)r * rc + i] = edge;
         } else {
           Pg[(size_t)r * rc + r] = corner;
+          if constexpr (SERVE) P[(size_t)r * rc + r] = corner;
         }
       }
       r += 1;
     }
     nobs += 1;
   }
+}
+
+template <typename REAL>
+__global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state st, const REAL* __restrict__ a_g,
+                                                     const REAL* __restrict__ y_g, rgb_logs logs,
+                                                     unsigned char* __restrict__ mirror,
+                                                     unsigned long long* __restrict__ dseq, REAL* __restrict__ hx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const R1Smem<REAL> S_(smem_raw, cfg);
+  const int m = cfg.m, k = cfg.k;
+  const bool onorm = cfg.variant == RGB_ORTHONORMAL;
+  const REAL* Cg = reinterpret_cast<const REAL*>(st.basis);
+  const REAL* Dg = onorm ? Cg : reinterpret_cast<const REAL*>(st.dual);
+  const REAL* Pg = reinterpret_cast<const REAL*>(st.gram_inv);
+  const REAL* Xg = reinterpret_cast<const REAL*>(st.x);
+  const int tid = threadIdx.x;
+  int r = st.rank[0];
+  int status = st.status[0];
+  int64_t nobs = st.nobs[0];
+  if (status) {
+    r1_publish<REAL>(mirror, dseq, nobs, r, status, tid);
+    return;
+  }
+  // ---- stage: the row and targets (host memory) first, then the state ------------
+  for (int j = tid; j < m; j += R1_NT) r1_cp(S_.a_s + j, a_g + j, sizeof(REAL));
+  for (int c = tid; c < k; c += R1_NT) r1_cp(S_.y_s + c, y_g + c, sizeof(REAL));
+  r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  row1_fold<REAL, false>(cfg, st, logs, S_, r, status, nobs, hx);
   if (tid == 0) {
     st.rank[0] = r;
     st.nobs[0] = nobs;
@@ -249,10 +307,116 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
   r1_publish<REAL>(mirror, dseq, nobs, r, status, tid);
 }
 
+#ifdef RGB_SERVE_PROBE
+__device__ unsigned long long g_sprobe[8];  // ns summed: poll, row read, fold, publish; rows
+__device__ __forceinline__ unsigned long long sp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPROBE(i)                                    \
+  do {                                               \
+    if (threadIdx.x == 0) {                          \
+      const unsigned long long n_ = sp_now();        \
+      atomicAdd(&g_sprobe[i], n_ - sp_t);            \
+      sp_t = n_;                                     \
+    }                                                \
+  } while (0)
+#else
+#define SPROBE(i) \
+  do {            \
+  } while (0)
+#endif
+
+// The row SERVER (rgb_rowpipe_run with a positive idle time): one persistent CTA
+// that stages the state once and then folds row after row.  Thread 0 polls the
+// request word of the mapped host block (acquire, system scope); a request is
+// the number of the row to fold (one more than the rows served, dseq); the row
+// and its targets are then read from the block with volatile loads (never from a
+// cache line of an earlier row), folded with row1_fold<SERVE> -- the same
+// arithmetic as row1_kernel, so results are bit-identical -- and published as
+// row1_kernel does.  The server exits on the stop word, after a stop status, or
+// after idle_ns without a request (the host relaunches it on demand).
+template <typename REAL>
+__global__ void __launch_bounds__(R1_NT) row1_serve_kernel(rgb_config cfg, rgb_state st,
+                                                           const REAL* __restrict__ a_g,
+                                                           const REAL* __restrict__ y_g, rgb_logs logs,
+                                                           unsigned char* __restrict__ mirror,
+                                                           unsigned long long* __restrict__ dseq,
+                                                           REAL* __restrict__ hx, unsigned long long idle_ns) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_cmd;
+  const R1Smem<REAL> S_(smem_raw, cfg);
+  const int m = cfg.m, k = cfg.k;
+  const bool onorm = cfg.variant == RGB_ORTHONORMAL;
+  const REAL* Cg = reinterpret_cast<const REAL*>(st.basis);
+  const REAL* Dg = onorm ? Cg : reinterpret_cast<const REAL*>(st.dual);
+  const REAL* Pg = reinterpret_cast<const REAL*>(st.gram_inv);
+  const REAL* Xg = reinterpret_cast<const REAL*>(st.x);
+  const int tid = threadIdx.x;
+  int r = st.rank[0];
+  int status = st.status[0];
+  int64_t nobs = st.nobs[0];
+  if (!status) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  const unsigned long long* req = reinterpret_cast<const unsigned long long*>(mirror + RGB_ROWPIPE_OFF_REQ);
+  const volatile unsigned* stop = reinterpret_cast<const volatile unsigned*>(mirror + RGB_ROWPIPE_OFF_STOP);
+  const volatile REAL* av = a_g;
+  const volatile REAL* yv = y_g;
+#ifdef RGB_SERVE_PROBE
+  unsigned long long sp_t = sp_now();
+#endif
+  while (true) {
+    if (tid == 0) {
+      const unsigned long long want = *dseq + 1;
+      unsigned long long t0, now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      int cmd = 0;
+      while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(req) : "memory");
+        if (v == want) {
+          cmd = 1;
+          break;
+        }
+        if (*stop) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (now - t0 > idle_ns) break;
+      }
+      s_cmd = cmd;
+    }
+    __syncthreads();
+    if (s_cmd != 1) return;
+    SPROBE(0);
+    if (!status) {  // (a state stopped earlier only publishes its counters, as row1_kernel)
+      for (int j = tid; j < m; j += R1_NT) S_.a_s[j] = av[j];
+      for (int c = tid; c < k; c += R1_NT) S_.y_s[c] = yv[c];
+      __syncthreads();
+      SPROBE(1);
+      row1_fold<REAL, true>(cfg, st, logs, S_, r, status, nobs, hx);
+      __syncthreads();
+      SPROBE(2);
+      if (tid == 0) {
+        st.rank[0] = r;
+        st.nobs[0] = nobs;
+        st.status[0] = status;
+      }
+    }
+    r1_publish<REAL>(mirror, dseq, nobs, r, status, tid);
+    SPROBE(3);
+#ifdef RGB_SERVE_PROBE
+    if (tid == 0) atomicAdd(&g_sprobe[4], 1ull);
+#endif
+    if (status) return;  // a stop: the host grows the capacity or reports it
+    __syncthreads();     // the request word is re-read only after every thread's publish path
+  }
+}
+
 static size_t row1_smem(const rgb_config& cfg) {
   const size_t es = cfg.dtype == RGB_F32 ? 4 : 8;
   const size_t m = cfg.m, rc = cfg.r_cap, k = cfg.k;
-  const size_t n = 2 * m + 2 * rc + R1_MK + R1_NW * (R1_MK + 2) +
+  const size_t n = 2 * m + 3 * rc + 2 * R1_MK + R1_NW * (R1_MK + 2) +
                    (cfg.variant == RGB_ORTHONORMAL ? 1 : 2) * rc * m + rc * rc + k * m;
   return n * es;
 }
@@ -269,6 +433,18 @@ static int launch_row1(const rgb_config& cfg, const rgb_state& st, const void* r
   kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
+
+template <typename REAL>
+static int launch_row1_serve(const rgb_config& cfg, const rgb_state& st, const void* rows, const void* tgts,
+                             const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, void* hx,
+                             unsigned long long idle_ns, cudaStream_t cs) {
+  const size_t smem = row1_smem(cfg);
+  if (smem > R1_MAXS) return RGB_E_UNSUPPORTED;
+  auto kern = row1_serve_kernel<REAL>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx, idle_ns);
+  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
 }  // namespace rgb
 
 struct rgb_rowpipe {
@@ -283,7 +459,40 @@ struct rgb_rowpipe {
   rgb_state st;
   rgb_logs logs;
   int64_t off_in = 0;
+  // row server (rgb_rowpipe_run with RGB_ROWSERVE_IDLE_US > 0): a persistent
+  // kernel on its own stream, launched on demand, that exits after idle_ns
+  bool serve_ok = false, serving = false;
+  unsigned long long idle_ns = 0;
+  cudaStream_t sstream = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::chrono::steady_clock::time_point last;
+  const void* rows = nullptr;
+  const void* tgts = nullptr;
 };
+
+// Stop the row server (if it runs) and wait for it: the state in global memory is
+// then final and the caller may run other kernels on it.
+static int serve_stop(rgb_rowpipe* p) {
+  if (!p->serving) return RGB_OK;
+  __atomic_store_n(reinterpret_cast<unsigned*>(p->host + RGB_ROWPIPE_OFF_STOP), 1u, __ATOMIC_RELEASE);
+  const cudaError_t e = cudaStreamSynchronize(p->sstream);
+  __atomic_store_n(reinterpret_cast<unsigned*>(p->host + RGB_ROWPIPE_OFF_STOP), 0u, __ATOMIC_RELEASE);
+  p->serving = false;
+  return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+}
+
+static int serve_launch(rgb_rowpipe* p, cudaStream_t caller) {
+  // ordered after the caller's earlier work on the state
+  if (cudaEventRecord(p->ev, caller) != cudaSuccess || cudaStreamWaitEvent(p->sstream, p->ev, 0) != cudaSuccess)
+    return RGB_E_CUDA;
+  const int rc = p->cfg.dtype == RGB_F64
+                     ? rgb::launch_row1_serve<double>(p->cfg, p->st, p->rows, p->tgts, p->logs, p->host_dev, p->dseq,
+                                                      p->hx_dev, p->idle_ns, p->sstream)
+                     : rgb::launch_row1_serve<float>(p->cfg, p->st, p->rows, p->tgts, p->logs, p->host_dev, p->dseq,
+                                                     p->hx_dev, p->idle_ns, p->sstream);
+  if (rc == RGB_OK) p->serving = true;
+  return rc;
+}
 
 static size_t align64(size_t v) { return (v + 63) & ~(size_t)63; }
 
@@ -304,6 +513,9 @@ int64_t rgb_rowpipe_layout(const rgb_config* cfg, int f32in, int64_t* off_in, in
 
 void rgb_rowpipe_destroy(rgb_rowpipe* p) {
   if (!p) return;
+  serve_stop(p);
+  if (p->sstream) cudaStreamDestroy(p->sstream);
+  if (p->ev) cudaEventDestroy(p->ev);
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->graph) cudaGraphDestroy(p->graph);
   if (p->dseq) cudaFree(p->dseq);
@@ -372,13 +584,74 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
     rgb_rowpipe_destroy(p);
     return rc != RGB_OK ? rc : RGB_E_CUDA;
   }
+  // the row server: where the one-row kernel applies (the state fits its shared memory)
+  p->rows = rows;
+  p->tgts = tgts;
+  const char* idle = getenv("RGB_ROWSERVE_IDLE_US");
+  const long idle_us = idle && idle[0] ? atol(idle) : 500;
+  if (idle_us > 0 && !f32in && cfg->k <= rgb::R1_MK && rgb::row1_smem(*cfg) <= rgb::R1_MAXS &&
+      cudaStreamCreateWithFlags(&p->sstream, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) == cudaSuccess) {
+    p->serve_ok = true;
+    p->idle_ns = (unsigned long long)idle_us * 1000ull;
+  }
+  cudaGetLastError();
   *out = p;
   *host_block = p->host;
   return RGB_OK;
 }
 
+int rgb_rowpipe_quiesce(rgb_rowpipe* p) {
+  if (!p) return RGB_E_INVALID;
+  return serve_stop(p);
+}
+
+static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
+  using clk = std::chrono::steady_clock;
+  const unsigned long long want = p->seq + 1;
+  if (p->serving) {
+    // surely still polling when the last row was served well within its idle time
+    // (its idle clock started before that row's publish was seen here)
+    const auto idle = std::chrono::nanoseconds((long long)p->idle_ns);
+    if (clk::now() - p->last > idle - std::chrono::microseconds(100)) {
+      const cudaError_t q = cudaStreamQuery(p->sstream);
+      if (q == cudaSuccess) p->serving = false;
+      else if (q != cudaErrorNotReady) return RGB_E_CUDA;
+    }
+  }
+  if (!p->serving) {
+    const int rc = serve_launch(p, caller);
+    if (rc != RGB_OK) return rc;
+  }
+  __atomic_store_n(reinterpret_cast<unsigned long long*>(p->host + RGB_ROWPIPE_OFF_REQ), want, __ATOMIC_RELEASE);
+  volatile unsigned long long* s = reinterpret_cast<volatile unsigned long long*>(p->host + RGB_ROWPIPE_OFF_SEQ);
+  for (long it = 0;; ++it) {
+    if (*s == want) break;
+    if (it < 4000) {
+      _mm_pause();
+      continue;
+    }
+    // the server may have timed out just before the request: relaunch it (it
+    // folds the pending request, whose number is one more than the rows served)
+    const cudaError_t q = cudaStreamQuery(p->sstream);
+    if (q == cudaSuccess && *s != want) {
+      p->serving = false;
+      const int rc = serve_launch(p, caller);
+      if (rc != RGB_OK) return rc;
+      it = 0;
+      continue;
+    }
+    if (q != cudaSuccess && q != cudaErrorNotReady) return RGB_E_CUDA;
+    sched_yield();
+  }
+  p->seq = want;
+  p->last = clk::now();
+  return RGB_OK;
+}
+
 int rgb_rowpipe_run(rgb_rowpipe* p, void* stream) {
   if (!p) return RGB_E_INVALID;
+  if (p->serve_ok) return serve_run(p, (cudaStream_t)stream);
   const unsigned long long want = p->seq + 1;
   const cudaError_t e = cudaGraphLaunch(p->exec, (cudaStream_t)stream);
   if (e != cudaSuccess) return RGB_E_CUDA;
@@ -401,3 +674,14 @@ int rgb_rowpipe_run(rgb_rowpipe* p, void* stream) {
 }
 
 }  // extern "C"
+
+#ifdef RGB_SERVE_PROBE
+extern "C" int rgb_serve_probe(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, rgb::g_sprobe, sizeof(rgb::g_sprobe));
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(rgb::g_sprobe, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

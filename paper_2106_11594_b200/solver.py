@@ -271,7 +271,7 @@ class RecursiveSolver:
         if A.shape[1] != self._m:
             raise ValueError(f"rows have {A.shape[1]} columns, expected {self._m}")
         y = self._kind.vector(targets, A.shape[0])
-        fast = self._fast.get(False) if self._fast else None
+        fast = self._fast.get(True) if self._fast else None  # the one pipe (its report goes unread)
         if A.shape[0] == 1 and fast is not None and fast[0] == self._st_key:
             _, pin, run, h, s, hdr_n, hdr_c = fast[:7]
             m = self._m
@@ -394,7 +394,7 @@ class RecursiveSolver:
         if n == 1 and not self._trackers and self._pipes is not None:
             # a per-row call: the row pipe (one graph launch; the kernel reads the
             # row from mapped host memory and writes the report back into it)
-            pipe = self._row_pipe(want_report)
+            pipe = self._row_pipe(True)  # one pipe per layout (one row server per state)
             if pipe is not None:
                 pipe["in"][:m] = A[0]
                 pipe["in"][m] = y[0]
@@ -411,6 +411,7 @@ class RecursiveSolver:
                                 "gain": pipe["gain"].copy()}
                     return {}
                 self._on_status(status)  # rank cap: grown; the row runs again below
+        self._quiesce()  # other kernels write the state: the row server stops first
         stream = torch.cuda.current_stream(bs.device)
         h = ctypes.c_void_p(stream.cuda_stream)
         cp = lib.rgb_memcpy_async
@@ -481,11 +482,14 @@ class RecursiveSolver:
 
     def _row_pipe(self, want_report):
         """The librgb row pipe of this solver's current layout (include/rgb.h,
-        rgb_rowpipe_*): a graph captured once whose kernel reads the staged
-        row from pinned, device-mapped host memory and writes the report and
-        the counters back, so update() costs one graph launch and a spin on a
-        sequence word.  Recreated when the state moves (capacity growth).
-        None (and pipes off) if creation fails."""
+        rgb_rowpipe_*): the row goes to a row server -- a one-CTA persistent
+        kernel that keeps the state in shared memory, reads the staged row from
+        pinned, device-mapped host memory and writes the report and the counters
+        back, so update() costs a request word and a spin on a sequence word; it
+        exits after RGB_ROWSERVE_IDLE_US (default 500 us) without a row and is
+        relaunched on demand (states beyond its shared memory: one graph launch
+        per row).  Recreated when the state moves (capacity growth).  None (and
+        pipes off) if creation fails."""
         bs = self._bs
         cfg, st = self._structs()
         key = (want_report, self._st_key)
@@ -523,6 +527,15 @@ class RecursiveSolver:
         self._fast[want_report] = (self._st_key, pipe["in"], lib.rgb_rowpipe_run, h, pipe["stream"], hdr["nobs"],
                                    hdr["cnt"], hdr["branch"], pipe["resid"], pipe["gain"])
         return pipe
+
+    def _quiesce(self):
+        """Stop the row pipe's row server (include/rgb.h, rgb_rowpipe_quiesce),
+        which keeps the state in its shared memory between update() calls,
+        before another kernel writes the state."""
+        if self._pipes:
+            lib = self._bs.lib
+            for pipe in self._pipes.values():
+                _lib.check(lib.rgb_rowpipe_quiesce(pipe["h"]), "rgb_rowpipe_quiesce")
 
     def _drop_pipes(self, keep=None):
         """Destroy the row pipes (all, or those not of layout `keep`)."""
