@@ -33,6 +33,10 @@ int launch_generic(const rgb_config& cfg, rgb_state& st, const void* rows, int64
 // the updated factors go straight to global memory: three barriers per row
 // instead of about ten plus a write-back pass.
 constexpr int R1_NT = 256, R1_NW = 8, R1_MK = 64;
+// the global-state kernels (states beyond shared memory) run 1 024 threads: their
+// phases stream the factors from L2, and more warps keep more loads in flight
+constexpr int R1_NT_GS = 1024;
+__host__ __device__ constexpr int r1_threads(bool gs) { return gs ? R1_NT_GS : R1_NT; }
 
 __device__ __forceinline__ void r1_cp(void* smem, const void* gmem, int bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -61,7 +65,8 @@ __device__ __forceinline__ void r1_publish(unsigned char* mirror, unsigned long 
 template <typename REAL>
 struct R1Smem {
   REAL *a_s, *rej_s, *gam, *z_s, *y_s, *red, *zd, *dyv, *D, *C, *P, *X;
-  __device__ R1Smem(unsigned char* raw, const rgb_config& cfg) {
+  // gst: the state stays in global memory (states beyond shared memory; L2-resident)
+  __device__ R1Smem(unsigned char* raw, const rgb_config& cfg, const rgb_state* gst = nullptr, int nw = R1_NW) {
     const int m = cfg.m, rc = cfg.r_cap;
     a_s = reinterpret_cast<REAL*>(raw);
     rej_s = a_s + m;
@@ -69,8 +74,15 @@ struct R1Smem {
     z_s = gam + rc;
     y_s = z_s + rc;
     red = y_s + R1_MK;                                       // [NW][MK + 2]
-    zd = red + R1_NW * (R1_MK + 2);                          // z / denom
+    zd = red + nw * (R1_MK + 2);                             // z / denom
     dyv = zd + rc;                                           // y - a.x (a-priori residuals)
+    if (gst) {
+      C = reinterpret_cast<REAL*>(gst->basis);
+      D = cfg.variant == RGB_ORTHONORMAL ? C : reinterpret_cast<REAL*>(gst->dual);
+      P = reinterpret_cast<REAL*>(gst->gram_inv);
+      X = reinterpret_cast<REAL*>(gst->x);
+      return;
+    }
     D = dyv + R1_MK;                                         // C~ rows < r
     C = cfg.variant == RGB_ORTHONORMAL ? D : D + (size_t)rc * m;  // C rows < r
     P = C + (size_t)rc * m;                                  // P^-1 [r][r] at stride rc
@@ -93,10 +105,31 @@ __device__ __forceinline__ void r1_stage_state(const rgb_config& cfg, const REAL
   for (int e = tid; e < k * m; e += R1_NT) r1_cp(S_.X + e, Xg + e, sizeof(REAL));
 }
 
+#ifdef RGB_SERVE_PROBE
+__device__ unsigned long long g_sprobe[16];  // ns summed: poll, row read, fold, publish; rows; fold phases A-D at 8..11
+__device__ __forceinline__ unsigned long long sp_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPROBE(i)                                    \
+  do {                                               \
+    if (threadIdx.x == 0) {                          \
+      const unsigned long long n_ = sp_now();        \
+      atomicAdd(&g_sprobe[i], n_ - sp_t);            \
+      sp_t = n_;                                     \
+    }                                                \
+  } while (0)
+#else
+#define SPROBE(i) \
+  do {            \
+  } while (0)
+#endif
+
 // The fold of the staged row (a_s, y_s) on the staged state, phases A-D: results
 // straight to global memory (and, for the row server, SERVE, into the staged
 // state too, which it keeps between rows).  r, status, nobs are updated.
-template <typename REAL, bool SERVE>
+template <typename REAL, bool SERVE, int NT>
 __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state& st, const rgb_logs& logs,
                                           const R1Smem<REAL>& S_, int& r, int& status, int64_t& nobs, REAL* hx) {
   const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
@@ -109,8 +142,11 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
   REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv);
   REAL* Xg = reinterpret_cast<REAL*>(st.x);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+#ifdef RGB_SERVE_PROBE
+  unsigned long long sp_t = sp_now();
+#endif
   // ---- A: coords (warp per dual row) and the |a|^2, a.x_c block partials ---------
-  for (int i = w; i < r; i += R1_NW) {
+  for (int i = w; i < r; i += (NT / 32)) {
     const REAL* d = D + (size_t)i * m;
     REAL s = 0;
     for (int j = lane; j < m; j += 32) s = fma(d[j], a_s[j], s);
@@ -120,19 +156,20 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
   for (int v = 1; v < 2 + k; ++v) {
     REAL s = 0;
     if (v == 1) {
-      for (int j = tid; j < m; j += R1_NT) s = fma(a_s[j], a_s[j], s);
+      for (int j = tid; j < m; j += NT) s = fma(a_s[j], a_s[j], s);
     } else {
       const REAL* xc = X + (size_t)(v - 2) * m;
-      for (int j = tid; j < m; j += R1_NT) s = fma(a_s[j], xc[j], s);
+      for (int j = tid; j < m; j += NT) s = fma(a_s[j], xc[j], s);
     }
     s = warp_sum(s);
     if (lane == 0) red[w * (R1_MK + 2) + v] = s;
   }
   __syncthreads();
+  SPROBE(8);
   // ---- B: rejection (thread per column) with its |rej|^2 partial; z = P^-1 coords
   {
     REAL s2 = 0;
-    for (int j = tid; j < m; j += R1_NT) {
+    for (int j = tid; j < m; j += NT) {
       REAL s = 0;
       for (int i = 0; i < r; ++i) s = fma(gam[i], C[(size_t)i * m + j], s);
       const REAL v = a_s[j] - s;
@@ -142,7 +179,7 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
     s2 = warp_sum(s2);
     if (lane == 0) red[w * (R1_MK + 2)] = s2;
   }
-  for (int i = w; i < r; i += R1_NW) {
+  for (int i = w; i < r; i += (NT / 32)) {
     const REAL* pr = P + (size_t)i * rc;
     REAL s = 0;
     for (int l = lane; l < r; l += 32) s = fma(pr[l], gam[l], s);
@@ -150,10 +187,11 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
     if (lane == 0) z_s[i] = s;
   }
   __syncthreads();
+  SPROBE(9);
   // ---- C: the sums (warp order), denom = 1 + coords.z, the rank test ---------------
   auto total = [&](int v) {
     REAL s = 0;
-    for (int q = 0; q < R1_NW; ++q) s += red[q * (R1_MK + 2) + v];
+    for (int q = 0; q < (NT / 32); ++q) s += red[q * (R1_MK + 2) + v];
     return s;
   };
   const REAL rej_sq = total(0), row_sq = total(1);
@@ -181,19 +219,20 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
   if (!status) {
     // a-priori residuals y_c - a.x_c and z / denom, once (the same bits as forming
     // them where used)
-    for (int c = tid; c < k; c += R1_NT) dyv[c] = y_s[c] - total(2 + c);
+    for (int c = tid; c < k; c += NT) dyv[c] = y_s[c] - total(2 + c);
     if (dep)
-      for (int i = tid; i < r; i += R1_NT) zd[i] = z_s[i] / denom;
+      for (int i = tid; i < r; i += NT) zd[i] = z_s[i] / denom;
     __syncthreads();
+    SPROBE(10);
     auto dy = [&](int c) { return dyv[c]; };
     if (tid == 0 && logs.branch) logs.branch[0] = dep ? 0 : 1;
     if (logs.resid)
-      for (int c = tid; c < k; c += R1_NT) reinterpret_cast<REAL*>(logs.resid)[c] = dy(c);
+      for (int c = tid; c < k; c += NT) reinterpret_cast<REAL*>(logs.resid)[c] = dy(c);
     REAL* gl = reinterpret_cast<REAL*>(logs.gain);
     // ---- D: the update, straight to global memory --------------------------------
     if (dep) {
       if (r > 0) {
-        for (int idx = tid; idx < r * r; idx += R1_NT) {
+        for (int idx = tid; idx < r * r; idx += NT) {
           const int i = idx / r, l = idx - i * r;
           const REAL zs = zd[l];
           REAL pv = P[(size_t)i * rc + l];
@@ -201,7 +240,7 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
           Pg[(size_t)i * rc + l] = pv;
           if constexpr (SERVE) P[(size_t)i * rc + l] = pv;
         }
-        for (int j = tid; j < m; j += R1_NT) {
+        for (int j = tid; j < m; j += NT) {
           REAL g = 0;
           for (int i = 0; i < r; ++i) g = fma(zd[i], D[(size_t)i * m + j], g);
           for (int c = 0; c < k; ++c) {
@@ -214,10 +253,10 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
           if (gl) gl[j] = g;
         }
       } else if (gl) {
-        for (int j = tid; j < m; j += R1_NT) gl[j] = 0;
+        for (int j = tid; j < m; j += NT) gl[j] = 0;
       }
     } else {
-      for (int j = tid; j < m; j += R1_NT) {
+      for (int j = tid; j < m; j += NT) {
         const REAL g = rej_s[j] / rej_sq;
         if (var == RGB_GENERAL) {
           for (int i = 0; i < r; ++i) {
@@ -249,7 +288,7 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
         }
         if (gl) gl[j] = g;
       }
-      for (int i = tid; i <= r; i += R1_NT) {
+      for (int i = tid; i <= r; i += NT) {
         REAL edge = 0, corner = 1;
         if (var != RGB_GENERAL) {
           if (i < r) edge = -(alpha * z_s[i]);
@@ -267,16 +306,22 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
       r += 1;
     }
     nobs += 1;
+#ifdef RGB_SERVE_PROBE
+    __syncthreads();
+#endif
+    SPROBE(11);
   }
 }
 
-template <typename REAL>
-__global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state st, const REAL* __restrict__ a_g,
+// GS: the state stays in global memory (no staging; the fold reads and writes it there)
+template <typename REAL, bool GS>
+__global__ void __launch_bounds__(r1_threads(GS), 1) row1_kernel(rgb_config cfg, rgb_state st, const REAL* __restrict__ a_g,
                                                      const REAL* __restrict__ y_g, rgb_logs logs,
                                                      unsigned char* __restrict__ mirror,
                                                      unsigned long long* __restrict__ dseq, REAL* __restrict__ hx) {
+  constexpr int NT = r1_threads(GS);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const R1Smem<REAL> S_(smem_raw, cfg);
+  const R1Smem<REAL> S_(smem_raw, cfg, GS ? &st : nullptr, NT / 32);
   const int m = cfg.m, k = cfg.k;
   const bool onorm = cfg.variant == RGB_ORTHONORMAL;
   const REAL* Cg = reinterpret_cast<const REAL*>(st.basis);
@@ -292,13 +337,13 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
     return;
   }
   // ---- stage: the row and targets (host memory) first, then the state ------------
-  for (int j = tid; j < m; j += R1_NT) r1_cp(S_.a_s + j, a_g + j, sizeof(REAL));
-  for (int c = tid; c < k; c += R1_NT) r1_cp(S_.y_s + c, y_g + c, sizeof(REAL));
-  r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
+  for (int j = tid; j < m; j += NT) r1_cp(S_.a_s + j, a_g + j, sizeof(REAL));
+  for (int c = tid; c < k; c += NT) r1_cp(S_.y_s + c, y_g + c, sizeof(REAL));
+  if (!GS) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
-  row1_fold<REAL, false>(cfg, st, logs, S_, r, status, nobs, hx);
+  row1_fold<REAL, false, NT>(cfg, st, logs, S_, r, status, nobs, hx);
   if (tid == 0) {
     st.rank[0] = r;
     st.nobs[0] = nobs;
@@ -307,26 +352,6 @@ __global__ void __launch_bounds__(R1_NT) row1_kernel(rgb_config cfg, rgb_state s
   r1_publish<REAL>(mirror, dseq, nobs, r, status, tid);
 }
 
-#ifdef RGB_SERVE_PROBE
-__device__ unsigned long long g_sprobe[8];  // ns summed: poll, row read, fold, publish; rows
-__device__ __forceinline__ unsigned long long sp_now() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define SPROBE(i)                                    \
-  do {                                               \
-    if (threadIdx.x == 0) {                          \
-      const unsigned long long n_ = sp_now();        \
-      atomicAdd(&g_sprobe[i], n_ - sp_t);            \
-      sp_t = n_;                                     \
-    }                                                \
-  } while (0)
-#else
-#define SPROBE(i) \
-  do {            \
-  } while (0)
-#endif
 
 // The row SERVER (rgb_rowpipe_run with a positive idle time): one persistent CTA
 // that stages the state once and then folds row after row.  Thread 0 polls the
@@ -337,16 +362,17 @@ __device__ __forceinline__ unsigned long long sp_now() {
 // arithmetic as row1_kernel, so results are bit-identical -- and published as
 // row1_kernel does.  The server exits on the stop word, after a stop status, or
 // after idle_ns without a request (the host relaunches it on demand).
-template <typename REAL>
-__global__ void __launch_bounds__(R1_NT) row1_serve_kernel(rgb_config cfg, rgb_state st,
+template <typename REAL, bool GS>
+__global__ void __launch_bounds__(r1_threads(GS), 1) row1_serve_kernel(rgb_config cfg, rgb_state st,
                                                            const REAL* __restrict__ a_g,
                                                            const REAL* __restrict__ y_g, rgb_logs logs,
                                                            unsigned char* __restrict__ mirror,
                                                            unsigned long long* __restrict__ dseq,
                                                            REAL* __restrict__ hx, unsigned long long idle_ns) {
+  constexpr int NT = r1_threads(GS);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_cmd;
-  const R1Smem<REAL> S_(smem_raw, cfg);
+  const R1Smem<REAL> S_(smem_raw, cfg, GS ? &st : nullptr, NT / 32);
   const int m = cfg.m, k = cfg.k;
   const bool onorm = cfg.variant == RGB_ORTHONORMAL;
   const REAL* Cg = reinterpret_cast<const REAL*>(st.basis);
@@ -357,7 +383,7 @@ __global__ void __launch_bounds__(R1_NT) row1_serve_kernel(rgb_config cfg, rgb_s
   int r = st.rank[0];
   int status = st.status[0];
   int64_t nobs = st.nobs[0];
-  if (!status) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
+  if (!status && !GS) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 0;\n" ::);
   const unsigned long long* req = reinterpret_cast<const unsigned long long*>(mirror + RGB_ROWPIPE_OFF_REQ);
@@ -390,11 +416,11 @@ __global__ void __launch_bounds__(R1_NT) row1_serve_kernel(rgb_config cfg, rgb_s
     if (s_cmd != 1) return;
     SPROBE(0);
     if (!status) {  // (a state stopped earlier only publishes its counters, as row1_kernel)
-      for (int j = tid; j < m; j += R1_NT) S_.a_s[j] = av[j];
-      for (int c = tid; c < k; c += R1_NT) S_.y_s[c] = yv[c];
+      for (int j = tid; j < m; j += NT) S_.a_s[j] = av[j];
+      for (int c = tid; c < k; c += NT) S_.y_s[c] = yv[c];
       __syncthreads();
       SPROBE(1);
-      row1_fold<REAL, true>(cfg, st, logs, S_, r, status, nobs, hx);
+      row1_fold<REAL, true, NT>(cfg, st, logs, S_, r, status, nobs, hx);
       __syncthreads();
       SPROBE(2);
       if (tid == 0) {
@@ -413,11 +439,12 @@ __global__ void __launch_bounds__(R1_NT) row1_serve_kernel(rgb_config cfg, rgb_s
   }
 }
 
-static size_t row1_smem(const rgb_config& cfg) {
+// shared memory of the row kernels: the scratch, plus the staged state unless gs
+static size_t row1_smem(const rgb_config& cfg, bool gs = false) {
   const size_t es = cfg.dtype == RGB_F32 ? 4 : 8;
   const size_t m = cfg.m, rc = cfg.r_cap, k = cfg.k;
-  const size_t n = 2 * m + 3 * rc + 2 * R1_MK + R1_NW * (R1_MK + 2) +
-                   (cfg.variant == RGB_ORTHONORMAL ? 1 : 2) * rc * m + rc * rc + k * m;
+  size_t n = 2 * m + 3 * rc + 2 * R1_MK + (r1_threads(gs) / 32) * (R1_MK + 2);
+  if (!gs) n += (cfg.variant == RGB_ORTHONORMAL ? 1 : 2) * rc * m + rc * rc + k * m;
   return n * es;
 }
 constexpr size_t R1_MAXS = 200 * 1024;
@@ -426,11 +453,13 @@ template <typename REAL>
 static int launch_row1(const rgb_config& cfg, const rgb_state& st, const void* rows, const void* tgts,
                        const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, void* hx,
                        cudaStream_t cs) {
-  const size_t smem = row1_smem(cfg);
+  // states beyond shared memory stay in global memory (L2-resident)
+  const bool gs = row1_smem(cfg) > R1_MAXS;
+  const size_t smem = row1_smem(cfg, gs);
   if (smem > R1_MAXS) return RGB_E_UNSUPPORTED;
-  auto kern = row1_kernel<REAL>;
+  auto kern = gs ? row1_kernel<REAL, true> : row1_kernel<REAL, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx);
+  kern<<<1, r1_threads(gs), smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
@@ -438,11 +467,13 @@ template <typename REAL>
 static int launch_row1_serve(const rgb_config& cfg, const rgb_state& st, const void* rows, const void* tgts,
                              const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, void* hx,
                              unsigned long long idle_ns, cudaStream_t cs) {
-  const size_t smem = row1_smem(cfg);
+  const bool gs = row1_smem(cfg) > R1_MAXS;
+  const size_t smem = row1_smem(cfg, gs);
   if (smem > R1_MAXS) return RGB_E_UNSUPPORTED;
-  auto kern = row1_serve_kernel<REAL>;
+  auto kern = gs ? row1_serve_kernel<REAL, true> : row1_serve_kernel<REAL, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<1, R1_NT, smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx, idle_ns);
+  kern<<<1, r1_threads(gs), smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx,
+                                       idle_ns);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 }  // namespace rgb
@@ -572,7 +603,7 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
       rc = cfg->dtype == RGB_F64
                ? rgb::launch_row1<double>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, p->hx_dev, cs)
                : rgb::launch_row1<float>(p->cfg, p->st, rows, tgts, p->logs, p->host_dev, p->dseq, p->hx_dev, cs);
-    if (rc == RGB_E_UNSUPPORTED)  // float rows into a double state, k > 64, states beyond shared memory
+    if (rc == RGB_E_UNSUPPORTED)  // float rows into a double state, k > 64, scratch beyond shared memory
       rc = rgb::launch_generic(p->cfg, p->st, rows, cfg->m, tgts, cfg->k, 1, p->logs, cs, nsm,
                                f32in && cfg->dtype == RGB_F64, p->host_dev, p->dseq, p->hx_dev);
     e = cudaStreamEndCapture(cs, &p->graph);
@@ -584,12 +615,13 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
     rgb_rowpipe_destroy(p);
     return rc != RGB_OK ? rc : RGB_E_CUDA;
   }
-  // the row server: where the one-row kernel applies (the state fits its shared memory)
+  // the row server: where the one-row kernel applies (same-type inputs, k <= 64; the
+  // state in shared memory when it fits, else in global memory)
   p->rows = rows;
   p->tgts = tgts;
   const char* idle = getenv("RGB_ROWSERVE_IDLE_US");
   const long idle_us = idle && idle[0] ? atol(idle) : 500;
-  if (idle_us > 0 && !f32in && cfg->k <= rgb::R1_MK && rgb::row1_smem(*cfg) <= rgb::R1_MAXS &&
+  if (idle_us > 0 && !f32in && cfg->k <= rgb::R1_MK && rgb::row1_smem(*cfg, true) <= rgb::R1_MAXS &&
       cudaStreamCreateWithFlags(&p->sstream, cudaStreamNonBlocking) == cudaSuccess &&
       cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming) == cudaSuccess) {
     p->serve_ok = true;
@@ -679,7 +711,7 @@ int rgb_rowpipe_run(rgb_rowpipe* p, void* stream) {
 extern "C" int rgb_serve_probe(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, rgb::g_sprobe, sizeof(rgb::g_sprobe));
   if (reset) {
-    unsigned long long z[8] = {};
+    unsigned long long z[16] = {};
     cudaMemcpyToSymbol(rgb::g_sprobe, z, sizeof(z));
   }
   return 0;

@@ -43,7 +43,7 @@ def _drive(m, idle_us, monkeypatch, seed=0, n=260):
     return s, view.copy(), out
 
 
-@pytest.mark.parametrize("m", [16, 128])
+@pytest.mark.parametrize("m", [16, 128, 1024])  # 1 024: the state stays in global memory
 def test_row_server_bit_identical_to_graph_path(m, monkeypatch):
     s1, v1, o1 = _drive(m, 400, monkeypatch)
     s0, v0, o0 = _drive(m, 0, monkeypatch)
