@@ -22,8 +22,12 @@
 // three grid barriers per 8 rows (U_b and the S / G W partials of P4 are formed
 // in P3 for every row of the tile and masked after the rank test, which leaves
 // the values of the masked computation unchanged; P6 waits for the next
-// projection's first barrier) instead of three-plus per row for a per-row
-// multi-SM scheme.  An independent row (solver.py:305-318) is applied by
+// projection's second barrier, its L2 loads beside the reduced G's) instead of
+// three-plus per row for a per-row multi-SM scheme -- and two for a tile of
+// dependent rows: when a projection ends, the next tile is staged (its rows come
+// into registers one tile ahead) and its P1 issued before the rank-test barrier,
+// which is then also the next tile's first barrier; a growth in between (the
+// basis moved) discards it.  An independent row (solver.py:305-318) is applied by
 // every CTA to its own columns / row block, and the rest of its tile is
 // re-projected.  The workspace (partials, barrier counter) is allocated per
 // call, stream-ordered on the caller's stream, so calls stay reentrant; it
@@ -109,8 +113,8 @@ struct GridSmem {
   double Gs[TT][GS];                   // full G of the tile (+ a.x0)
   double Ps[8][PS];                    // my row block of P^-1
   double Wb[8][8];                     // my row block of W (c = column)
-  double At[TT][AS];                   // the tile's rows, my columns
-  double Yv[TT][8];                    // targets of the tile
+  double At[2][TT][AS];                // the tile's rows, my columns (two tiles: the next
+  double Yv[2][TT][8];                 // one is staged for the speculative projection); targets
   double Rs[TT][CW];                   // rejections of my columns
   double red[NW][TT * CW > 128 ? TT * CW : 128];  // per-warp partials
   double Ub[8][8], Eb[8][8], Dy[8][8], Yb[8][8];
@@ -242,6 +246,53 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       const int t = tid >> 3, cc = tid & 7;
       ny = (tid < 64 && tile < ntiles && t0 + t < T && cc < k) ? (double)__ldg(Yb + (t0 + t) * k + cc) : 0.0;
     };
+    // stage the registers (the next tile) into At / Yv buffer s
+    auto stage = [&](int s) {
+#pragma unroll
+      for (int i = 0; i < PA; ++i) {
+        const int e = tid + NT * i;
+        if (e < TT * CW) S.At[s][e / CW][e % CW] = na[i];
+      }
+      if (tid < 64) S.Yv[s][tid >> 3][tid & 7] = ny;
+    };
+    // P1: G partial of my columns for the tile in At buffer s (M = t, N = i, K = my
+    // columns) -> ws_g, and its |a_t|^2 partials -> ws_rp (N tiles past the rank are
+    // zero: skipped here, zeroed by the reducers)
+    auto p1 = [&](int s, double* ws_rp) {
+      const int nlive = (r + 7) >> 3;
+      for (int n0 = w; n0 < NXT; n0 += 4 * NW) {
+        double acc[4][2] = {};
+        bool on[4];
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int nt = n0 + NW * jj;
+          on[jj] = nt < NXT && (nt >= IT || nt < nlive);
+        }
+#pragma unroll
+        for (int kt = 0; kt < CW / 4; ++kt) {
+          const double a = S.At[s][p][4 * kt + q];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (on[jj]) mma(acc[jj], a, S.Ds[n0 + NW * jj][kt][lane]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          if (on[jj])
+            *reinterpret_cast<double2*>(ws_g + ((size_t)c * TT + p) * GX + 8 * (n0 + NW * jj) + 2 * q) =
+                make_double2(acc[jj][0], acc[jj][1]);
+      }
+      if (tid < TT) {  // |a_t|^2 of my columns
+        double sa = 0.0;
+        for (int j = 0; j < CW; ++j) sa = fma(S.At[s][tid][j], S.At[s][tid][j], sa);
+        ws_rp[((size_t)1 * TT + tid) * nc + c] = sa;
+      }
+    };
+    // speculation: when the projection of a tile ends, the next tile is staged and
+    // its P1 issued before the rank-test barrier (C~ does not change unless the
+    // test finds an independent row); the next tile then starts at its second
+    // barrier -- two grid barriers per dependent tile instead of three
+    int cur = 0;
+    bool staged = false, spec_valid = false;
     load_next(0);
     for (int64_t tile = 0; tile < ntiles && !stopped; ++tile) {
       const int64_t t0 = tile * TT;
@@ -250,54 +301,34 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
       // elapsed time until the stream's rank first reaches its final value's tile
       if (threadIdx.x == 0 && blockIdx.x < 2 && tile == (int64_t)(R / 8)) g_gprobe[blockIdx.x][12] = ggtime() - probe_t0;
 #endif
-      // tile rows of my columns and the targets (loaded one tile ahead)
-#pragma unroll
-      for (int i = 0; i < PA; ++i) {
-        const int e = tid + NT * i;
-        if (e < TT * CW) S.At[e / CW][e % CW] = na[i];
+      // tile rows of my columns and the targets (loaded one tile ahead); a tile
+      // staged already by the previous tile's speculative projection is used as
+      // it is, and its projection too when no growth came in between
+      bool skip_p1 = false;
+      if (staged) {
+        cur ^= 1;
+        staged = false;
+        skip_p1 = spec_valid;
+      } else {
+        stage(cur);
+        load_next(tile + 1);
+        __syncthreads();
       }
-      if (tid < 64) S.Yv[tid >> 3][tid & 7] = ny;
-      load_next(tile + 1);
-      __syncthreads();
+      spec_valid = false;
       int row_start = 0;
       while (true) {
         // a tile whose rows are all independent runs no barrier between the
         // test's reads of ws_r and the next projection's writes: alternate buffers
         double* ws_r = ws_r0 + (size_t)(nproj++ & 1u) * nc * 2 * TT;
         const bool bulk_try = bulk && row_start == 0 && tv == TT && r + TT <= rc;
-        // ---- P1: G partial of my columns (M = t, N = i, K = my columns) -> ws
-        // (N tiles past the rank are zero: skipped here, zeroed by the reducers)
         const int nlive = (r + 7) >> 3;
-        for (int n0 = w; n0 < NXT; n0 += 4 * NW) {
-          double acc[4][2] = {};
-          bool on[4];
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int nt = n0 + NW * jj;
-            on[jj] = nt < NXT && (nt >= IT || nt < nlive);
-          }
-#pragma unroll
-          for (int kt = 0; kt < CW / 4; ++kt) {
-            const double a = S.At[p][4 * kt + q];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              if (on[jj]) mma(acc[jj], a, S.Ds[n0 + NW * jj][kt][lane]);
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            if (on[jj])
-              *reinterpret_cast<double2*>(ws_g + ((size_t)c * TT + p) * GX + 8 * (n0 + NW * jj) + 2 * q) =
-                  make_double2(acc[jj][0], acc[jj][1]);
+        if (!skip_p1) {  // (else issued by the previous tile's speculation)
+          p1(cur, ws_r);
+          GPROBE(0);
+          grid_sync(ctr, epoch);
+          GPROBE(1);
         }
-        if (tid < TT) {  // |a_t|^2 of my columns
-          double s = 0.0;
-          for (int j = 0; j < CW; ++j) s = fma(S.At[tid][j], S.At[tid][j], s);
-          ws_r[((size_t)1 * TT + tid) * nc + c] = s;
-        }
-        GPROBE(0);
-        grid_sync(ctr, epoch);
-        GPROBE(1);
-        if (pending_p6) apply_p6();
+        skip_p1 = false;
         // ---- P2: G = sum of the partials.  CTA c reduces a contiguous chunk of
         // elements: warp w reads partials u = w, w+8, ... (coalesced rows of
         // 32 elements), then the 8 warp sums are added in a fixed order.
@@ -349,6 +380,9 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             const int e = tid + NT * i;
             v[i] = e < TT * GX ? __ldcg(ws_gf + e) : 0.0;
           }
+          // meanwhile P_b -= Y_b D^-1 Y^T of the last fold: every owner's Y rows are in
+          // (written before this barrier) and P_b is next read by U_b below
+          if (pending_p6) apply_p6();
 #pragma unroll
           for (int i = 0; i < PER; ++i) {
             const int e = tid + NT * i;
@@ -388,7 +422,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
           __syncthreads();
           for (int e = tid; e < TT * CW; e += NT) {
-            double v = S.At[e / CW][e % CW];
+            double v = S.At[cur][e / CW][e % CW];
 #pragma unroll
             for (int u = 0; u < NW; ++u) v += S.red[u][e];
             S.Rs[e / CW][e % CW] = v;
@@ -442,6 +476,16 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2) * 64 + p * 8 + 2 * q) = make_double2(sp[0], sp[1]);
             *reinterpret_cast<double2*>(ws_s + ((size_t)c * 2 + 1) * 64 + p * 8 + 2 * q) = make_double2(gw[0], gw[1]);
           }
+        }
+        if (!bulk && tile + 1 < ntiles) {
+          if (!staged) {
+            stage(cur ^ 1);
+            load_next(tile + 2);
+            staged = true;
+          }
+          __syncthreads();
+          p1(cur ^ 1, ws_r0 + (size_t)(nproj & 1u) * nc * 2 * TT);
+          spec_valid = true;
         }
         GPROBE(4);
         grid_sync(ctr, epoch);
@@ -538,7 +582,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             const double mtt = (t & 1) ? y1 : y0;
             const double at = S.red[0][TT + t];
             bool yok = true;
-            for (int cc = 0; cc < k; ++cc) yok &= isfinite(S.Yv[t][cc]);
+            for (int cc = 0; cc < k; ++cc) yok &= isfinite(S.Yv[cur][t][cc]);
             const double dt = 1.0 / rdt;
             const double e2 = eps_sq<double>(cfg, r + t);
             const bool ok = isfinite(at) && yok && dt > BULK_COND * mtt && dt > BULK_MARGIN * e2 * fmax(1.0, at);
@@ -584,7 +628,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             }
             for (int e = tid; e < tst * CW; e += NT) {
               const int t = e / CW, jl = e % CW, i = r + t;
-              S.Cs[i >> 2][jl >> 3][4 * (jl & 7) + (i & 3)] = -S.At[t][jl];
+              S.Cs[i >> 2][jl >> 3][4 * (jl & 7) + (i & 3)] = -S.At[cur][t][jl];
             }
             if (owner) {
               // P = diag(P, I); W gains rows y_t - a_t.x0 (a.x0 = 0 here)
@@ -595,7 +639,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               }
               if (tid < 64) {
                 const int i = 8 * c + (tid >> 3), cc = tid & 7;
-                if (i >= r && i < r + tst) S.Wb[tid >> 3][cc] = cc < k ? S.Yv[i - r][cc] - S.Gs[i - r][R + cc] : 0.0;
+                if (i >= r && i < r + tst) S.Wb[tid >> 3][cc] = cc < k ? S.Yv[cur][i - r][cc] - S.Gs[i - r][R + cc] : 0.0;
               }
             }
             if (c == 0) {
@@ -607,6 +651,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             }
             __syncthreads();
             r += tst;
+            spec_valid = false;  // the basis moved: a speculative next-tile projection is stale
             if (tst >= tv) break;    // the whole tile grew
             row_start = tst;         // the rest of the tile: re-projected on the new basis
             continue;
@@ -618,7 +663,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           const double asq = lane < TT ? S.red[0][TT + lane] : 0.0;
           bool ybad = false;
           if (lane < TT)
-            for (int cc = 0; cc < k; ++cc) ybad |= !isfinite(S.Yv[lane][cc]);
+            for (int cc = 0; cc < k; ++cc) ybad |= !isfinite(S.Yv[cur][lane][cc]);
           const bool valid = lane >= row_start && lane < tv;
           const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
           const bool bad = !isfinite(asq) || ybad;
@@ -670,7 +715,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               if (p == 2 * q + 1) mi[1] += 1.0;
 #pragma unroll
               for (int e = 0; e < 2; ++e)  // dy0[t = p][cc = 2q + e]
-                S.Dy[p][2 * q + e] = in_r ? S.Yv[p][2 * q + e] - S.Gs[p][R + 2 * q + e] - gws[e] : 0.0;
+                S.Dy[p][2 * q + e] = in_r ? S.Yv[cur][p][2 * q + e] - S.Gs[p][R + 2 * q + e] - gws[e] : 0.0;
               double ev[2] = {p == 2 * q ? 1.0 : 0.0, p == 2 * q + 1 ? 1.0 : 0.0};
 #pragma unroll
               for (int kk = 0; kk < TT - 1; ++kk) {
@@ -754,7 +799,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
           for (int e = tid; e < CW; e += NT) {
             const int kt = r >> 2, nt = e >> 3, l = 4 * (e & 7) + (r & 3);
-            S.Cs[kt][nt][l] = -S.At[ts][e];
+            S.Cs[kt][nt][l] = -S.At[cur][ts][e];
           }
           if (owner) {
             // P = diag(P, 1); W gains row r = y - a.x0 of row ts
@@ -763,7 +808,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
               if (i == r || i2 == r) S.Ps[e / R][i2] = (i == i2) ? 1.0 : 0.0;
             }
             if ((r >> 3) == c && tid < 8)
-              S.Wb[r & 7][tid] = tid < k ? S.Yv[ts][tid] - S.Gs[ts][R + tid] : 0.0;
+              S.Wb[r & 7][tid] = tid < k ? S.Yv[cur][ts][tid] - S.Gs[ts][R + tid] : 0.0;
           }
           if (c == 0 && tid == 0) {
             const int64_t row = b * T + t0 + ts;
@@ -773,6 +818,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
           __syncthreads();
           r += 1;
+          spec_valid = false;  // the basis moved: a speculative next-tile projection is stale
         } else {
           if (pending_p6) {  // z = P gamma needs the folded P
             grid_sync(ctr, epoch);
@@ -834,7 +880,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
             if (rown && tid < 8) {
               double gw = 0.0;
               for (int u = 0; u < IT; ++u) gw += __ldcg(ws_d + (size_t)u * 16 + 1 + tid);
-              S.Wb[r & 7][tid] = tid < k ? alpha * ((S.Yv[ts][tid] - S.Gs[ts][R + tid]) - gw) : 0.0;
+              S.Wb[r & 7][tid] = tid < k ? alpha * ((S.Yv[cur][ts][tid] - S.Gs[ts][R + tid]) - gw) : 0.0;
             }
           }
           if (c == 0 && tid == 0) {
@@ -845,6 +891,7 @@ __global__ void __launch_bounds__(NT, 1) grid_kernel(rgb_config cfg, rgb_state s
           }
           __syncthreads();
           r += 1;
+          spec_valid = false;  // the basis moved: a speculative next-tile projection is stale
         }
         row_start = tstar + 1;
         if (row_start >= tv) break;
