@@ -172,6 +172,8 @@ int rgb_covariance(const rgb_config *cfg, const rgb_state *state, void *out, voi
 #define RGB_ROWPIPE_OFF_BRANCH 24
 #define RGB_ROWPIPE_OFF_REQ 32  /* u64: row server request (the row number), written by rgb_rowpipe_run */
 #define RGB_ROWPIPE_OFF_STOP 40 /* u32: row server stop word, written by rgb_rowpipe_quiesce */
+#define RGB_ROWPIPE_OFF_PREQ 48 /* u64: projection request number, written by rgb_rowpipe_project */
+#define RGB_ROWPIPE_OFF_PSEQ 56 /* u64: the projection last served (written by the server) */
 typedef struct rgb_rowpipe rgb_rowpipe;
 
 /* Size of a row pipe's host block (bytes) and the offsets of its areas. */
@@ -192,6 +194,13 @@ int rgb_rowpipe_create(const rgb_config *cfg, const rgb_state *state, int want_r
  * at create; default 500, 0 = one graph launch per row).  It is launched on
  * demand, ordered after the work already on `stream`. */
 int rgb_rowpipe_run(rgb_rowpipe *pipe, void *stream);
+/* Project the row staged in the block's input area on the current basis
+ * (RecursiveSolver.project, solver.py:210-219) through the row server, without
+ * touching the state: coords [r_cap] (zero past the rank), rejection [m] and
+ * |rejection|^2 (the state's type) at rgb_rowpipe_proj_offset.  Blocks until they
+ * are visible; RGB_E_UNSUPPORTED when the pipe has no row server. */
+int rgb_rowpipe_project(rgb_rowpipe *pipe, void *stream);
+int64_t rgb_rowpipe_proj_offset(const rgb_config *cfg, int f32in);
 /* Stop the pipe's row server (if it runs) and wait for it: call before any
  * other kernel writes the state (an ingest of several rows, a reset).
  * rgb_rowpipe_destroy stops it too. */

@@ -25,10 +25,11 @@ EXPORTS = ("rgb_abi_version", "rgb_last_error", "rgb_state_reset", "rgb_ingest",
            "rgb_memcpy_async",
            "rgb_project", "rgb_pinv", "rgb_covariance",
            "rgb_rowpipe_layout", "rgb_rowpipe_create", "rgb_rowpipe_run", "rgb_rowpipe_quiesce",
-           "rgb_rowpipe_destroy")
+           "rgb_rowpipe_destroy", "rgb_rowpipe_project", "rgb_rowpipe_proj_offset")
 # row pipe host-block header (include/rgb.h)
 ROWPIPE_HEADER, ROWPIPE_OFF_SEQ, ROWPIPE_OFF_NOBS, ROWPIPE_OFF_RANK = 64, 0, 8, 16
 ROWPIPE_OFF_STATUS, ROWPIPE_OFF_BRANCH, ROWPIPE_OFF_REQ, ROWPIPE_OFF_STOP = 20, 24, 32, 40
+ROWPIPE_OFF_PREQ, ROWPIPE_OFF_PSEQ = 48, 56
 
 
 class Config(ctypes.Structure):
@@ -100,10 +101,13 @@ def load():
                                        ctypes.POINTER(vp)]
     lib.rgb_rowpipe_run.argtypes = [vp, vp]
     lib.rgb_rowpipe_quiesce.argtypes = [vp]
+    lib.rgb_rowpipe_project.argtypes = [vp, vp]
+    lib.rgb_rowpipe_proj_offset.argtypes = [cfgp, ctypes.c_int]
     lib.rgb_rowpipe_destroy.argtypes = [vp]
     for name in EXPORTS[2:]:
         getattr(lib, name).restype = ctypes.c_int
     lib.rgb_rowpipe_layout.restype = ctypes.c_int64
+    lib.rgb_rowpipe_proj_offset.restype = ctypes.c_int64
     lib.rgb_rowpipe_destroy.restype = None
     if lib.rgb_abi_version() != RGB_ABI_VERSION:
         raise RgbError(f"librgb.so ABI {lib.rgb_abi_version()} != {RGB_ABI_VERSION}")

@@ -129,22 +129,16 @@ __device__ __forceinline__ unsigned long long sp_now() {
 // The fold of the staged row (a_s, y_s) on the staged state, phases A-D: results
 // straight to global memory (and, for the row server, SERVE, into the staged
 // state too, which it keeps between rows).  r, status, nobs are updated.
-template <typename REAL, bool SERVE, int NT>
-__device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state& st, const rgb_logs& logs,
-                                          const R1Smem<REAL>& S_, int& r, int& status, int64_t& nobs, REAL* hx) {
-  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
-  const bool onorm = var == RGB_ORTHONORMAL;
-  REAL *a_s = S_.a_s, *rej_s = S_.rej_s, *gam = S_.gam, *z_s = S_.z_s, *y_s = S_.y_s, *red = S_.red;
-  REAL *zd = S_.zd, *dyv = S_.dyv;
-  REAL *D = S_.D, *C = S_.C, *P = S_.P, *X = S_.X;
-  REAL* Cg = reinterpret_cast<REAL*>(st.basis);
-  REAL* Dg = onorm ? Cg : reinterpret_cast<REAL*>(st.dual);
-  REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv);
-  REAL* Xg = reinterpret_cast<REAL*>(st.x);
+// Phases A and B of the fold -- the projection of the staged row a_s on the staged
+// basis (solver.py:286-291): coords gam (warp per dual row), the rejection rej_s
+// (thread per column) and per-warp partials of |rej|^2 (red[w][0]), |a|^2 (red[w][1])
+// and a.x_c (red[w][2 + c]); z = P^-1 coords (z_s).  Ends with a CTA barrier.
+template <typename REAL, int NT>
+__device__ __forceinline__ void row1_ab(const rgb_config& cfg, const R1Smem<REAL>& S_, int r) {
+  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap;
+  const REAL *a_s = S_.a_s, *D = S_.D, *C = S_.C, *P = S_.P, *X = S_.X;
+  REAL *rej_s = S_.rej_s, *gam = S_.gam, *z_s = S_.z_s, *red = S_.red;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-#ifdef RGB_SERVE_PROBE
-  unsigned long long sp_t = sp_now();
-#endif
   // ---- A: coords (warp per dual row) and the |a|^2, a.x_c block partials ---------
   for (int i = w; i < r; i += (NT / 32)) {
     const REAL* d = D + (size_t)i * m;
@@ -165,7 +159,6 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
     if (lane == 0) red[w * (R1_MK + 2) + v] = s;
   }
   __syncthreads();
-  SPROBE(8);
   // ---- B: rejection (thread per column) with its |rej|^2 partial; z = P^-1 coords
   {
     REAL s2 = 0;
@@ -187,6 +180,25 @@ __device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state
     if (lane == 0) z_s[i] = s;
   }
   __syncthreads();
+}
+
+template <typename REAL, bool SERVE, int NT>
+__device__ __forceinline__ void row1_fold(const rgb_config& cfg, const rgb_state& st, const rgb_logs& logs,
+                                          const R1Smem<REAL>& S_, int& r, int& status, int64_t& nobs, REAL* hx) {
+  const int m = cfg.m, k = cfg.k, rc = cfg.r_cap, var = cfg.variant;
+  const bool onorm = var == RGB_ORTHONORMAL;
+  REAL *a_s = S_.a_s, *rej_s = S_.rej_s, *gam = S_.gam, *z_s = S_.z_s, *y_s = S_.y_s, *red = S_.red;
+  REAL *zd = S_.zd, *dyv = S_.dyv;
+  REAL *D = S_.D, *C = S_.C, *P = S_.P, *X = S_.X;
+  REAL* Cg = reinterpret_cast<REAL*>(st.basis);
+  REAL* Dg = onorm ? Cg : reinterpret_cast<REAL*>(st.dual);
+  REAL* Pg = reinterpret_cast<REAL*>(st.gram_inv);
+  REAL* Xg = reinterpret_cast<REAL*>(st.x);
+  const int tid = threadIdx.x, lane = tid & 31;
+#ifdef RGB_SERVE_PROBE
+  unsigned long long sp_t = sp_now();
+#endif
+  row1_ab<REAL, NT>(cfg, S_, r);
   SPROBE(9);
   // ---- C: the sums (warp order), denom = 1 + coords.z, the rank test ---------------
   auto total = [&](int v) {
@@ -368,7 +380,8 @@ __global__ void __launch_bounds__(r1_threads(GS), 1) row1_serve_kernel(rgb_confi
                                                            const REAL* __restrict__ y_g, rgb_logs logs,
                                                            unsigned char* __restrict__ mirror,
                                                            unsigned long long* __restrict__ dseq,
-                                                           REAL* __restrict__ hx, unsigned long long idle_ns) {
+                                                           REAL* __restrict__ hx, REAL* __restrict__ proj,
+                                                           unsigned long long idle_ns) {
   constexpr int NT = r1_threads(GS);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_cmd;
@@ -383,10 +396,12 @@ __global__ void __launch_bounds__(r1_threads(GS), 1) row1_serve_kernel(rgb_confi
   int r = st.rank[0];
   int status = st.status[0];
   int64_t nobs = st.nobs[0];
-  if (!status && !GS) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);
+  if (!GS) r1_stage_state<REAL>(cfg, Cg, Dg, Pg, Xg, S_, r);  // (a stopped state still projects)
   asm volatile("cp.async.commit_group;\n" ::);
   asm volatile("cp.async.wait_group 0;\n" ::);
   const unsigned long long* req = reinterpret_cast<const unsigned long long*>(mirror + RGB_ROWPIPE_OFF_REQ);
+  const unsigned long long* preq = reinterpret_cast<const unsigned long long*>(mirror + RGB_ROWPIPE_OFF_PREQ);
+  __shared__ unsigned long long s_preq;
   const volatile unsigned* stop = reinterpret_cast<const volatile unsigned*>(mirror + RGB_ROWPIPE_OFF_STOP);
   const volatile REAL* av = a_g;
   const volatile REAL* yv = y_g;
@@ -398,12 +413,21 @@ __global__ void __launch_bounds__(r1_threads(GS), 1) row1_serve_kernel(rgb_confi
       const unsigned long long want = *dseq + 1;
       unsigned long long t0, now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      // the projection served last is the one whose number the block's PSEQ word holds
+      const unsigned long long pdone =
+          *reinterpret_cast<volatile const unsigned long long*>(mirror + RGB_ROWPIPE_OFF_PSEQ);
       int cmd = 0;
       while (true) {
         unsigned long long v;
         asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(req) : "memory");
         if (v == want) {
           cmd = 1;
+          break;
+        }
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(preq) : "memory");
+        if (v != pdone) {
+          cmd = 2;
+          s_preq = v;
           break;
         }
         if (*stop) break;
@@ -413,6 +437,26 @@ __global__ void __launch_bounds__(r1_threads(GS), 1) row1_serve_kernel(rgb_confi
       s_cmd = cmd;
     }
     __syncthreads();
+    if (s_cmd == 2) {
+      // project() (solver.py:210-219): coords, rejection and |rej|^2 of the staged row on
+      // the current basis -- phases A and B of the fold, nothing written to the state
+      for (int j = tid; j < m; j += NT) S_.a_s[j] = av[j];
+      __syncthreads();
+      row1_ab<REAL, NT>(cfg, S_, r);
+      for (int i = tid; i < cfg.r_cap; i += NT) proj[i] = i < r ? S_.gam[i] : (REAL)0;
+      for (int j = tid; j < m; j += NT) proj[cfg.r_cap + j] = S_.rej_s[j];
+      if (tid == 0) {
+        REAL s = 0;
+        for (int q = 0; q < NT / 32; ++q) s += S_.red[q * (R1_MK + 2)];  // warp order, as the fold
+        proj[cfg.r_cap + m] = s;
+      }
+      __syncthreads();
+      if (tid == 0)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(mirror + RGB_ROWPIPE_OFF_PSEQ), "l"(s_preq)
+                     : "memory");
+      __syncthreads();
+      continue;
+    }
     if (s_cmd != 1) return;
     SPROBE(0);
     if (!status) {  // (a state stopped earlier only publishes its counters, as row1_kernel)
@@ -466,14 +510,14 @@ static int launch_row1(const rgb_config& cfg, const rgb_state& st, const void* r
 template <typename REAL>
 static int launch_row1_serve(const rgb_config& cfg, const rgb_state& st, const void* rows, const void* tgts,
                              const rgb_logs& logs, unsigned char* mirror, unsigned long long* dseq, void* hx,
-                             unsigned long long idle_ns, cudaStream_t cs) {
+                             void* proj, unsigned long long idle_ns, cudaStream_t cs) {
   const bool gs = row1_smem(cfg) > R1_MAXS;
   const size_t smem = row1_smem(cfg, gs);
   if (smem > R1_MAXS) return RGB_E_UNSUPPORTED;
   auto kern = gs ? row1_serve_kernel<REAL, true> : row1_serve_kernel<REAL, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kern<<<1, r1_threads(gs), smem, cs>>>(cfg, st, (const REAL*)rows, (const REAL*)tgts, logs, mirror, dseq, (REAL*)hx,
-                                       idle_ns);
+                                       (REAL*)proj, idle_ns);
   return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 }  // namespace rgb
@@ -489,7 +533,7 @@ struct rgb_rowpipe {
   rgb_config cfg;
   rgb_state st;
   rgb_logs logs;
-  int64_t off_in = 0;
+  int64_t off_in = 0, off_proj = 0;
   // row server (rgb_rowpipe_run with RGB_ROWSERVE_IDLE_US > 0): a persistent
   // kernel on its own stream, launched on demand, that exits after idle_ns
   bool serve_ok = false, serving = false;
@@ -499,6 +543,7 @@ struct rgb_rowpipe {
   std::chrono::steady_clock::time_point last;
   const void* rows = nullptr;
   const void* tgts = nullptr;
+  unsigned long long pseq = 0;  // projections requested so far
 };
 
 // Stop the row server (if it runs) and wait for it: the state in global memory is
@@ -518,9 +563,9 @@ static int serve_launch(rgb_rowpipe* p, cudaStream_t caller) {
     return RGB_E_CUDA;
   const int rc = p->cfg.dtype == RGB_F64
                      ? rgb::launch_row1_serve<double>(p->cfg, p->st, p->rows, p->tgts, p->logs, p->host_dev, p->dseq,
-                                                      p->hx_dev, p->idle_ns, p->sstream)
+                                                      p->hx_dev, p->host_dev + p->off_proj, p->idle_ns, p->sstream)
                      : rgb::launch_row1_serve<float>(p->cfg, p->st, p->rows, p->tgts, p->logs, p->host_dev, p->dseq,
-                                                     p->hx_dev, p->idle_ns, p->sstream);
+                                                     p->hx_dev, p->host_dev + p->off_proj, p->idle_ns, p->sstream);
   if (rc == RGB_OK) p->serving = true;
   return rc;
 }
@@ -536,10 +581,19 @@ int64_t rgb_rowpipe_layout(const rgb_config* cfg, int f32in, int64_t* off_in, in
   const size_t in = RGB_ROWPIPE_HEADER;
   const size_t resid = align64(in + ies * ((size_t)cfg->m + cfg->k));
   const size_t gain = align64(resid + es * (size_t)cfg->k);
+  const size_t proj = align64(gain + es * (size_t)cfg->m);  // rgb_rowpipe_proj_offset
   if (off_in) *off_in = (int64_t)in;
   if (off_resid) *off_resid = (int64_t)resid;
   if (off_gain) *off_gain = (int64_t)gain;
-  return (int64_t)align64(gain + es * (size_t)cfg->m);
+  return (int64_t)align64(proj + es * ((size_t)cfg->r_cap + cfg->m + 1));
+}
+
+int64_t rgb_rowpipe_proj_offset(const rgb_config* cfg, int f32in) {
+  int64_t off_gain = 0;
+  const int64_t bytes = rgb_rowpipe_layout(cfg, f32in, nullptr, nullptr, &off_gain);
+  if (bytes < 0) return bytes;
+  const size_t es = cfg->dtype == RGB_F32 ? 4 : 8;
+  return (int64_t)align64((size_t)off_gain + es * (size_t)cfg->m);
 }
 
 void rgb_rowpipe_destroy(rgb_rowpipe* p) {
@@ -584,6 +638,7 @@ int rgb_rowpipe_create(const rgb_config* cfg, const rgb_state* st, int want_repo
     p->logs.gain = p->host_dev + off_gain;
   }
   p->off_in = off_in;
+  p->off_proj = rgb_rowpipe_proj_offset(cfg, f32in);
   int nsm = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -638,12 +693,12 @@ int rgb_rowpipe_quiesce(rgb_rowpipe* p) {
   return serve_stop(p);
 }
 
-static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
+// a server that is surely still polling, or a new one (ordered after `caller`)
+static int serve_ensure(rgb_rowpipe* p, cudaStream_t caller) {
   using clk = std::chrono::steady_clock;
-  const unsigned long long want = p->seq + 1;
   if (p->serving) {
-    // surely still polling when the last row was served well within its idle time
-    // (its idle clock started before that row's publish was seen here)
+    // surely still polling when the last request was served well within its idle time
+    // (its idle clock started before that request's publish was seen here)
     const auto idle = std::chrono::nanoseconds((long long)p->idle_ns);
     if (clk::now() - p->last > idle - std::chrono::microseconds(100)) {
       const cudaError_t q = cudaStreamQuery(p->sstream);
@@ -651,12 +706,17 @@ static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
       else if (q != cudaErrorNotReady) return RGB_E_CUDA;
     }
   }
-  if (!p->serving) {
-    const int rc = serve_launch(p, caller);
-    if (rc != RGB_OK) return rc;
-  }
-  __atomic_store_n(reinterpret_cast<unsigned long long*>(p->host + RGB_ROWPIPE_OFF_REQ), want, __ATOMIC_RELEASE);
-  volatile unsigned long long* s = reinterpret_cast<volatile unsigned long long*>(p->host + RGB_ROWPIPE_OFF_SEQ);
+  return p->serving ? RGB_OK : serve_launch(p, caller);
+}
+
+// post request `want` at the block's word `off_req` and spin until the server
+// publishes it at `off_done`
+static int serve_request(rgb_rowpipe* p, cudaStream_t caller, size_t off_req, size_t off_done,
+                         unsigned long long want) {
+  int rc = serve_ensure(p, caller);
+  if (rc != RGB_OK) return rc;
+  __atomic_store_n(reinterpret_cast<unsigned long long*>(p->host + off_req), want, __ATOMIC_RELEASE);
+  volatile unsigned long long* s = reinterpret_cast<volatile unsigned long long*>(p->host + off_done);
   for (long it = 0;; ++it) {
     if (*s == want) break;
     if (it < 4000) {
@@ -664,11 +724,12 @@ static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
       continue;
     }
     // the server may have timed out just before the request: relaunch it (it
-    // folds the pending request, whose number is one more than the rows served)
+    // serves the pending request: a row whose number is one more than the rows
+    // served, a projection whose number differs from the last one published)
     const cudaError_t q = cudaStreamQuery(p->sstream);
     if (q == cudaSuccess && *s != want) {
       p->serving = false;
-      const int rc = serve_launch(p, caller);
+      rc = serve_launch(p, caller);
       if (rc != RGB_OK) return rc;
       it = 0;
       continue;
@@ -676,9 +737,24 @@ static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
     if (q != cudaSuccess && q != cudaErrorNotReady) return RGB_E_CUDA;
     sched_yield();
   }
-  p->seq = want;
-  p->last = clk::now();
+  p->last = std::chrono::steady_clock::now();
   return RGB_OK;
+}
+
+static int serve_run(rgb_rowpipe* p, cudaStream_t caller) {
+  const unsigned long long want = p->seq + 1;
+  const int rc = serve_request(p, caller, RGB_ROWPIPE_OFF_REQ, RGB_ROWPIPE_OFF_SEQ, want);
+  if (rc == RGB_OK) p->seq = want;
+  return rc;
+}
+
+int rgb_rowpipe_project(rgb_rowpipe* p, void* stream) {
+  if (!p) return RGB_E_INVALID;
+  if (!p->serve_ok) return RGB_E_UNSUPPORTED;
+  const unsigned long long want = p->pseq + 1;
+  const int rc = serve_request(p, (cudaStream_t)stream, RGB_ROWPIPE_OFF_PREQ, RGB_ROWPIPE_OFF_PSEQ, want);
+  if (rc == RGB_OK) p->pseq = want;
+  return rc;
 }
 
 int rgb_rowpipe_run(rgb_rowpipe* p, void* stream) {

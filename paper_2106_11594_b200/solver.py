@@ -194,8 +194,21 @@ class RecursiveSolver:
 
     # -- core operations ------------------------------------------------------
     def project(self, row):
-        """Coordinates of ``row`` in the stored basis plus its rejection."""
+        """Coordinates of ``row`` in the stored basis plus its rejection
+        (solver.py:210-219): through the row server when the solver has one (the
+        state is already in its shared memory), else one projection kernel."""
         row = self._kind.vector(row, self._m)
+        if not self._trackers and self._pipes is not None:
+            pipe = self._row_pipe(True)
+            if pipe is not None and pipe.get("proj") is not None:
+                m = self._m
+                pipe["in"][:m] = row
+                rc = self._bs.lib.rgb_rowpipe_project(pipe["h"], pipe["stream"])
+                if rc == _lib.OK:
+                    pc, pr, ps = pipe["proj"]
+                    return ProjectionResult(pc[:self.rank].copy(), pr.copy(), float(ps[0]))
+                if rc != _lib.E_UNSUPPORTED:
+                    _lib.check(rc, "rgb_rowpipe_project")
         torch = self._torch
         bs = self._bs
         m, rc = self._m, bs.r_cap
@@ -512,7 +525,11 @@ class RecursiveSolver:
         idt = np.dtype(np.float32) if (self._f32in or sdt == np.float32) else np.dtype(np.float64)
         o_in, o_res, o_gain = (o.value for o in off)
         m = self._m
-        pipe = {"h": h, "raw": raw,
+        off_p = lib.rgb_rowpipe_proj_offset(ctypes.byref(cfg), int(self._f32in))
+        rc_, esz = bs.r_cap, sdt.itemsize
+        proj = (raw[off_p:off_p + esz * rc_].view(sdt), raw[off_p + esz * rc_:off_p + esz * (rc_ + m)].view(sdt),
+                raw[off_p + esz * (rc_ + m):off_p + esz * (rc_ + m + 1)].view(sdt))
+        pipe = {"h": h, "raw": raw, "proj": proj,
                 # every drop-in call completes before it returns, so one stream
                 # handle per pipe is safe
                 "stream": ctypes.c_void_p(self._torch.cuda.current_stream(bs.device).cuda_stream),

@@ -1,6 +1,6 @@
 """Per-call latency of the drop-in per-row API (RecursiveSolver.update, and
 ingest / project of one row) against the reference's own update
-(baseline/_ref, the unmodified rankrls, one core), with the distribution
+and project (baseline/_ref, the unmodified rankrls, one core), with the distribution
 (median / p90 / p99) and a breakdown of one update() call: the graph replay +
 synchronisation alone, and the device time of the captured work.
 
@@ -33,13 +33,17 @@ def reference_update(m, A, rows, ys, r):
 
     s = rs.RecursiveSolver(m)
     s.ingest(A[:r], np.zeros(r))
-    ts = []
+    ts, tp = [], []
     for i in range(len(rows)):
         t0 = time.perf_counter()
         s.update(rows[i], ys[i])
         ts.append(time.perf_counter() - t0)
+    for i in range(len(rows)):
+        t0 = time.perf_counter()
+        s.project(rows[i])
+        tp.append(time.perf_counter() - t0)
     sys.path.remove(ref)
-    return dist(ts[20:])
+    return dist(ts[20:]), dist(tp[20:])
 
 
 def main():
@@ -77,7 +81,8 @@ def main():
                 lib.rgb_rowpipe_run(pipe["h"], h)
                 ts.append(time.perf_counter() - t0)
             res["rowpipe_run"] = dist(ts[20:])
-        res["reference_update"] = reference_update(m, A, rows[:200], ys[:200], r)
+        ref = reference_update(m, A, rows[:200], ys[:200], r)
+        res["reference_update"], res["reference_project"] = ref if ref else (None, None)
         out[f"m={m}"] = res
         print(f"m={m}", json.dumps(res), flush=True)
     if len(sys.argv) > 1:

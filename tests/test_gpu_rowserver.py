@@ -84,3 +84,39 @@ def test_row_server_state_visible_to_other_kernels(monkeypatch):
     x = oracle.solution(o)[0, :, 0]
     assert np.abs(s.solution - x).max() <= 1e-9 * max(1.0, np.abs(x).max())
     assert pr.coords.shape == (12,)
+
+
+@pytest.mark.parametrize("m", [16, 128, 1024])
+def test_project_through_row_server(m, monkeypatch):
+    """project() (solver.py:210-219) goes to the row server when the solver has one:
+    the same coords / rejection as the projection kernel (RGB_ROWSERVE_IDLE_US=0)
+    to rounding, nothing written to the state, and is_dependent(project(a), a)
+    (solver.py:221-229) predicts update(a)'s branch."""
+    import paper_2106_11594_b200 as p
+
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((12, m))
+    probe = np.vstack([rng.standard_normal((6, 12)) @ A, rng.standard_normal((6, m))])  # dependent, independent
+
+    def run(idle):
+        monkeypatch.setenv("RGB_ROWSERVE_IDLE_US", str(idle))
+        s = p.RecursiveSolver(m)
+        for i in range(12):
+            s.update(A[i], float(i))
+        x0 = s.solution.copy()
+        projs = [s.project(a) for a in probe]
+        assert np.array_equal(s.solution, x0) and s.num_observations == 12  # state untouched
+        return s, projs
+
+    s1, p1 = run(400)
+    s0, p0 = run(0)
+    for a, x, y in zip(probe, p1, p0):
+        scale = max(1.0, float(np.abs(a).max()))
+        assert x.coords.shape == y.coords.shape == (min(12, m),)
+        assert np.abs(x.coords - y.coords).max() <= 1e-11 * max(1.0, np.abs(y.coords).max())
+        assert np.abs(x.rejection - y.rejection).max() <= 1e-11 * scale
+        assert abs(x.rejection_sq_norm - y.rejection_sq_norm) <= 1e-10 * scale * scale
+    for a in probe:  # project, test, then fold: the test predicts the fold's branch
+        dep = s1.is_dependent(s1.project(a), a)
+        rep = s1.update(a, 0.0)
+        assert (rep.branch == "dependent") == dep
