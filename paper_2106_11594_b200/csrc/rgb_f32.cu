@@ -33,10 +33,11 @@ namespace f32k {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int M = 64, R = 16, KX = 8, TT = 8, WARPS = 4, NT = WARPS * 32;
 constexpr int PS = 20;  // padded row pitch of P^-1 (conflict-light row reads)
+constexpr int AP = M + 4;  // row pitch of the tile ring: conflict-free 8-byte MMA fragment reads
 constexpr int GS = 28;  // row pitch of G: 16 coordinates + 8 a.x0 columns + pad
 
 struct __align__(16) WarpSmem {
-  float A[2][TT][M];    // tile ring (cp.async)
+  float A[2][TT][AP];   // tile ring (cp.async)
   float Y[2][TT][KX];   // targets ring
   float G[TT][GS];      // G | a.x0
   float P[R][PS];       // P^-1
@@ -57,6 +58,21 @@ __device__ __forceinline__ float rcpf(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
+}
+
+// 3xTF32: x = big + small with big = x rounded to tf32 (cvt.rna) and small = x - big
+// (exact; the tensor core reads its top 10 mantissa bits), so that
+// big_a big_b + big_a small_b + small_a big_b carries fp32-level accuracy
+__device__ __forceinline__ void tf32_split(float x, uint32_t& big, uint32_t& small) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(big) : "f"(x));
+  small = __float_as_uint(x - __uint_as_float(big));
+}
+// D += A B on mma.sync m16n8k8 (tf32 in, fp32 accumulate)
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 
 __device__ __forceinline__ void cp4(void* smem, const void* gmem, bool ok) {
@@ -152,6 +168,7 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
   const int64_t gw = (int64_t)blockIdx.x * WARPS + wib, nw = (int64_t)gridDim.x * WARPS;
   const int j0 = lane, j1 = lane + 32;  // my columns
   const int pi = lane & 15, ph = lane >> 4;  // my (row, half) in the 16 x 16 / 16 x 8 matrices
+  const int fg = lane >> 2, fq = lane & 3;    // my MMA fragment coordinates
 
   for (int64_t b = gw; b < cfg.num_streams; b += nw) {
     int status = st.status[b];
@@ -168,16 +185,20 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
     if (ntiles > 0) stage_tile(S, 0, Rb, Yb, T, k, 0, lane);
 
     // ---- load the state: C~, C (my columns), x0 (my columns), P^-1; W = 0 ----
-    // C~: lane (pi, ph) holds row pi, columns [32 ph, 32 ph + 32) (G partials need
-    // only a pair reduction); C: lane l holds columns l and l + 32 of every row (R is lane-local)
-    float Dr[32], Ct[R][2];
+    // C~: the A fragments of G^T = C~ A^T on mma.sync m16n8k8 (M = rank, K = column):
+    // lane (fg, fq) holds rows fg and fg + 8 at columns 8kk + 2fq + {0, 1}, kk < 8
+    // (logical K slots fq and fq + 4 of k-step kk); C: lane l holds columns l and
+    // l + 32 of every row (R is lane-local)
+    float Dm[8][4], Ct[R][2];
 #pragma unroll
-    for (int q = 0; q < 32; q += 4) {
-      const float4 v = pi < r ? *reinterpret_cast<const float4*>(Dg + pi * M + 32 * ph + q) : make_float4(0, 0, 0, 0);
-      Dr[q] = v.x;
-      Dr[q + 1] = v.y;
-      Dr[q + 2] = v.z;
-      Dr[q + 3] = v.w;
+    for (int kk = 0; kk < 8; ++kk) {
+      const float2 v0 = fg < r ? *reinterpret_cast<const float2*>(Dg + fg * M + 8 * kk + 2 * fq) : make_float2(0, 0);
+      const float2 v1 =
+          fg + 8 < r ? *reinterpret_cast<const float2*>(Dg + (fg + 8) * M + 8 * kk + 2 * fq) : make_float2(0, 0);
+      Dm[kk][0] = v0.x;
+      Dm[kk][1] = v1.x;
+      Dm[kk][2] = v0.y;
+      Dm[kk][3] = v1.y;
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) {
@@ -229,35 +250,29 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
       }
       int row_start = 0;
       while (true) {
-        // ---- G = A C~^T: lane (pi, ph) sums row pi of C~ against the tile's rows over
-        // its 32 columns (broadcast shared-memory reads), then one pair reduction
+        // ---- G = A C~^T on the tensor cores: G^T = C~ A^T (M = rank, N = the tile's
+        // rows, K = columns), tf32 in three passes (big x big, then big x small and
+        // small x big into a second accumulator), fp32 accumulation
         {
-          float g[TT];
+          float gb[4] = {0.f, 0.f, 0.f, 0.f}, gsm[4] = {0.f, 0.f, 0.f, 0.f};
+          const float* arow = &S.A[s][fg][2 * fq];
 #pragma unroll
-          for (int t = 0; t < TT; ++t) {
-            const float4* ar = reinterpret_cast<const float4*>(&S.A[s][t][32 * ph]);
-            float acc0 = 0.f, acc1 = 0.f;
+          for (int kk = 0; kk < 8; ++kk) {
+            const float2 bv = *reinterpret_cast<const float2*>(arow + 8 * kk);
+            uint32_t bb[2], bs[2], ab[4], as[4];
+            tf32_split(bv.x, bb[0], bs[0]);
+            tf32_split(bv.y, bb[1], bs[1]);
 #pragma unroll
-            for (int q = 0; q < 8; q += 2) {
-              const float4 x = ar[q], y = ar[q + 1];
-              acc0 = fmaf(x.x, Dr[4 * q], acc0);
-              acc1 = fmaf(y.x, Dr[4 * q + 4], acc1);
-              acc0 = fmaf(x.y, Dr[4 * q + 1], acc0);
-              acc1 = fmaf(y.y, Dr[4 * q + 5], acc1);
-              acc0 = fmaf(x.z, Dr[4 * q + 2], acc0);
-              acc1 = fmaf(y.z, Dr[4 * q + 6], acc1);
-              acc0 = fmaf(x.w, Dr[4 * q + 3], acc0);
-              acc1 = fmaf(y.w, Dr[4 * q + 7], acc1);
-            }
-            g[t] = acc0 + acc1;
+            for (int e = 0; e < 4; ++e) tf32_split(Dm[kk][e], ab[e], as[e]);
+            mma_tf32(gb, ab, bb);
+            mma_tf32(gsm, ab, bs);
+            mma_tf32(gsm, as, bb);
           }
-#pragma unroll
-          for (int t = 0; t < TT; ++t) {
-            const float other = __shfl_xor_sync(FULL, g[t], 16);
-            g[t] = ph ? other + g[t] : g[t] + other;  // the same order in both lanes of the pair
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) S.G[4 * ph + u][pi] = g[4 * ph + u];
+          // G^T[fg][2fq], G^T[fg][2fq + 1], G^T[fg + 8][2fq], G^T[fg + 8][2fq + 1]
+          S.G[2 * fq][fg] = gb[0] + gsm[0];
+          S.G[2 * fq + 1][fg] = gb[1] + gsm[1];
+          S.G[2 * fq][fg + 8] = gb[2] + gsm[2];
+          S.G[2 * fq + 1][fg + 8] = gb[3] + gsm[3];
         }
         if (has_x0) {  // a.x0_c (continuation calls): 2 more reduce-scatters
 #pragma unroll
@@ -540,22 +555,24 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
               Ct[i][1] = ats1;
             }
           __syncwarp();
-          {  // C~[:r] -= gamma K^T, C~[r] = K on my row / half
-            const float gi = S.G[ts][pi];
-            const float4* kr = reinterpret_cast<const float4*>(&S.Kv[32 * ph]);
+          {  // C~[:r] -= gamma K^T, C~[r] = K on my fragment rows fg, fg + 8
+            const float gi0 = S.G[ts][fg], gi1 = S.G[ts][fg + 8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 kq = kr[q];
-              if (pi < r) {
-                Dr[4 * q] = fmaf(-gi, kq.x, Dr[4 * q]);
-                Dr[4 * q + 1] = fmaf(-gi, kq.y, Dr[4 * q + 1]);
-                Dr[4 * q + 2] = fmaf(-gi, kq.z, Dr[4 * q + 2]);
-                Dr[4 * q + 3] = fmaf(-gi, kq.w, Dr[4 * q + 3]);
-              } else if (pi == r) {
-                Dr[4 * q] = kq.x;
-                Dr[4 * q + 1] = kq.y;
-                Dr[4 * q + 2] = kq.z;
-                Dr[4 * q + 3] = kq.w;
+            for (int kk = 0; kk < 8; ++kk) {
+              const float2 kq = *reinterpret_cast<const float2*>(&S.Kv[8 * kk + 2 * fq]);
+              if (fg < r) {
+                Dm[kk][0] = fmaf(-gi0, kq.x, Dm[kk][0]);
+                Dm[kk][2] = fmaf(-gi0, kq.y, Dm[kk][2]);
+              } else if (fg == r) {
+                Dm[kk][0] = kq.x;
+                Dm[kk][2] = kq.y;
+              }
+              if (fg + 8 < r) {
+                Dm[kk][1] = fmaf(-gi1, kq.x, Dm[kk][1]);
+                Dm[kk][3] = fmaf(-gi1, kq.y, Dm[kk][3]);
+              } else if (fg + 8 == r) {
+                Dm[kk][1] = kq.x;
+                Dm[kk][3] = kq.y;
               }
             }
           }
@@ -582,12 +599,14 @@ __global__ void __launch_bounds__(NT, RGB_F32_MINB) f32_kernel(rgb_config cfg, r
 
     // ---- write back C~, C, P^-1; x = x0 + C~^T W ---------------------------------------
     // (C~ is staged in the tile ring so that column owners can form x)
-    float* Dsm = &S.A[0][0][0];  // 16 x 64 floats = the two tile slots
+    float* Dsm = &S.A[0][0][0];  // 16 x 64 floats within the two tile slots
 #pragma unroll
-    for (int q = 0; q < 32; q += 4) {
-      const float4 v = make_float4(Dr[q], Dr[q + 1], Dr[q + 2], Dr[q + 3]);
-      *reinterpret_cast<float4*>(Dsm + pi * M + 32 * ph + q) = v;
-      if (pi < rc) *reinterpret_cast<float4*>(Dg + pi * M + 32 * ph + q) = v;
+    for (int kk = 0; kk < 8; ++kk) {
+      const float2 v0 = make_float2(Dm[kk][0], Dm[kk][2]), v1 = make_float2(Dm[kk][1], Dm[kk][3]);
+      *reinterpret_cast<float2*>(Dsm + fg * M + 8 * kk + 2 * fq) = v0;
+      *reinterpret_cast<float2*>(Dsm + (fg + 8) * M + 8 * kk + 2 * fq) = v1;
+      if (fg < rc) *reinterpret_cast<float2*>(Dg + fg * M + 8 * kk + 2 * fq) = v0;
+      if (fg + 8 < rc) *reinterpret_cast<float2*>(Dg + (fg + 8) * M + 8 * kk + 2 * fq) = v1;
     }
 #pragma unroll
     for (int i = 0; i < R; ++i)
