@@ -1173,6 +1173,42 @@ def test_large_stream_kernels_interleaved_dependent_rows(m, r_cap, r, n, variant
     assert relerr(res["coords"][0], o["coords"][0]) <= 1e-9
 
 
+@pytest.mark.parametrize("variant,alpha", [("general", 1.0), ("orthogonal", 0.7), ("orthonormal", 1.0)])
+def test_grid_kernel_growth_after_speculated_tiles(variant, alpha):
+    """The grid kernel issues the next tile's projection before the rank-test
+    barrier when a projection ends (rgb_grid.cu, speculative P1).  Independent rows
+    placed exactly at tile boundaries after fully dependent tiles (the speculation
+    is taken, then its tile grows at row 0 and the speculation issued during it
+    is discarded) and mid-tile, against the oracle's branches, factors and x."""
+    m, r_cap = 2048, 64
+    rng = np.random.default_rng(5)
+    basis = rng.standard_normal((40, m))
+    grow_at = {32, 45, 64, 72, 103, 128, 129, 160}
+    rows, seen, nxt = [], [], 0
+    for t in range(200):
+        if t < 8 or t in grow_at:
+            rows.append(basis[nxt])
+            seen.append(nxt)
+            nxt += 1
+        else:
+            rows.append(rng.standard_normal(len(seen)) @ basis[seen])
+    rows = np.ascontiguousarray(np.array(rows))
+    tg = rng.standard_normal((len(rows), 1))
+    res = run_batched(rows, tg, r_cap=r_cap, variant=variant, alpha=alpha)
+    o = oracle.ingest(rows[None], tg[None], r_cap=r_cap, variant=variant, alpha=alpha)
+    assert res["status"][0] == 0
+    r = int(o["rank"][0])
+    assert int(res["rank"][0]) == r == nxt
+    assert np.array_equal(np.nonzero(o["branch"][0])[0], np.array(sorted(set(range(8)) | grow_at)))
+    assert np.array_equal(res["branch"][0], o["branch"][0])
+    assert relerr(res["x"][0], oracle.solution(o)[0]) <= 1e-10
+    bs = res["solver"]
+    assert relerr(bs.basis_t[0, :r].cpu().numpy(), o["C"][0, :r]) <= 1e-10
+    D = bs.dual_t[0, :r].cpu().numpy()
+    assert relerr(D, (o["C"] if variant == "orthonormal" else o["D"])[0, :r]) <= 1e-10
+    assert relerr(bs.gram_t[0, :r, :r].cpu().numpy(), o["P"][0, :r, :r]) <= 1e-8
+
+
 # -- update() fold against ingest() (ADVICE r1) ---------------------------------------
 
 @pytest.mark.parametrize("m,n", [(128, 300), (1024, 160)])
