@@ -164,7 +164,7 @@ class ClockSampler:
 
 def fp64_peak():
     """Live peaks of this GPU (tools/libfp64peak.so), TFLOP/s: fp64 DFMA and DMMA,
-    and fp32 FFMA (the fp32-state kernel's pipe)."""
+    fp32 FFMA (the fp32-state kernel's pipe) and tf32 mma.sync (its G projection)."""
     import ctypes
 
     from paper_2106_11594_b200 import _build
@@ -173,7 +173,7 @@ def fp64_peak():
         lib = ctypes.CDLL(_build.build_peak_probe())
         lib.rgb_probe_fp64_peak.restype = ctypes.c_double
         return {"dfma": lib.rgb_probe_fp64_peak(0), "dmma": lib.rgb_probe_fp64_peak(1),
-                "ffma": lib.rgb_probe_fp64_peak(2)}
+                "ffma": lib.rgb_probe_fp64_peak(2), "tf32_mma": lib.rgb_probe_fp64_peak(3)}
     except Exception as e:  # noqa: BLE001
         return {"error": str(e)}
 
@@ -545,7 +545,9 @@ def run_ours(args):
                          "traffic": ncu_traffic(args.config, args.dtype),
                          "algorithmic_flops_per_launch": flops_total / world,
                          "kernel_ms": kern_ms, "peak_source": peak_src,
-                         "note": (("bound by the fp32 CUDA-core pipe (FFMA; the fp32-state kernel rgb_f32.cu); "
+                         "note": (("bound by the fp32 CUDA-core pipe (FFMA; the fp32-state kernel rgb_f32.cu, whose "
+                                   "G = A C~^T runs as 3-pass tf32 on mma.sync: fp64_peaks_tflops.tf32_mma / 3 is that "
+                                   "path's fp32-accurate ceiling); "
                                    if args.dtype == "fp32-state" else
                                    "bound by the fp64 tensor pipe (mma.sync DMMA; tcgen05 has no f64 kind); ") +
                                   "achieved counts the reference's per-row op count (SURVEY.md 8(d)) over the branch "
