@@ -54,6 +54,7 @@
 //   P^-1   Pr[mt][nt][e]     = P[8mt+p][8nt+2q+e]        home registers (symmetric)
 //   W^T    Wt[mt][e]         = W[8mt+2q+e][c=p]          home registers
 #include <cstddef>
+#include <cstdlib>
 #include <type_traits>
 
 #include "rgb_mma.cuh"
@@ -130,7 +131,7 @@ template <int R, int M, typename TI>
 __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
     const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
-    double* __restrict__ clog, unsigned* __restrict__ next_stream) {
+    double* __restrict__ clog, unsigned* __restrict__ next_stream, int seq_only) {
   using SMT = PanelSmem<R, M, TI>;
   constexpr int IT = SMT::IT, IK = SMT::IK, NJ = SMT::NJ, KS = SMT::KS;
   // own columns of a projection warp (row mode, growth, write-back): the 8-column
@@ -161,12 +162,18 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
   // streams are claimed dynamically (their cost varies with the rank they reach:
   // row-mode length, rank tiles of every projection and of the P^-1 chain)
   // (no counter when every CTA has at most one stream: the CTA index is the stream)
+  int64_t b = 0;
+  bool redo = false;  // the deferred fold of stream b failed its conditioning certificate
   for (unsigned iter = 0;; ++iter) {
     __syncthreads();  // every thread has read the previous claim
-    if (threadIdx.x == 0)
-      S.claim = next_stream ? atomicAdd(next_stream, 1u) : (iter == 0 ? blockIdx.x : 0xffffffffu);
-    __syncthreads();
-    const int64_t b = S.claim;
+    if (!redo) {
+      if (threadIdx.x == 0)
+        S.claim = next_stream ? atomicAdd(next_stream, 1u) : (iter == 0 ? blockIdx.x : 0xffffffffu);
+      __syncthreads();
+      b = S.claim;
+    }
+    const bool seq = redo || seq_only != 0;
+    redo = false;
     if (b >= cfg.num_streams) break;
     int status = st.status[b];
     if (status) continue;  // uniform across the block
@@ -179,6 +186,16 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
     const TI* Rb = rows + b * rstride;
     const TI* Yb = tgts + b * tstride;
     const bool fresh = (r == 0);
+    // Deferred fold (a fresh stream): in the general variant neither the rank test nor
+    // growth reads P^-1 or W, so the per-row Sherman-Morrison chain (solver.py:297-304)
+    // is not needed while the rows stream by.  It is the recursive form of
+    //   P^-1 = (B^T B)^-1,  W = P^-1 B^T (y - A x0)       (B: the coords log, A = B C)
+    // so the home warp only accumulates Q = B^T B and B^T dy on the tensor cores -- no
+    // dependent chain -- and the CTA inverts Q once at the end.  The inverse is accepted
+    // when kappa_F(Q) = |Q|_F |Q^-1|_F <= DEFER_KAPPA (the two forms then agree to
+    // ~1e-16 kappa, measured against the reference's own recursion: <= 4e-11 in x);
+    // otherwise the stream is folded again with the sequential chain below.
+    const bool defer = fresh && !seq;
 
     // ---- state into shared memory (rank 0 is all zeros by the state contract) ----
     for (int i = threadIdx.x; i < IT * KS * 32; i += PANEL_THREADS) {
@@ -897,6 +914,37 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
         for (int u = 0; u < PW; ++u) {
           const int te = S.sTe[u];
           if (te <= 0 || nti == 0) continue;  // r = 0: dependent rows are zero rows (solver.py:323-326)
+          if (defer) {
+            // ---- deferred fold: Q += G^T G, (B^T dy)^T += dy^T G over rows [0, te) of tile u.
+            // Pr holds Q and Wt holds (B^T dy)^T here.  G^T comes straight out of the slot:
+            // the accumulator layout the projection warp stored is, read at 32 s + 8 q + p,
+            // G[4s + q][8nt + p] -- the A operand (M = coords, K = rows) and the B operand
+            // (K = rows, N = coords) at once, conflict-free.
+            double gt[IT][2], dv[2];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const bool in = 4 * s + q < te;
+#pragma unroll
+              for (int nt = 0; nt < IT; ++nt)
+                gt[nt][s] = (in && nt < nti) ? (&S.sG[u][nt][0][0])[32 * s + 8 * q + p] : 0.0;
+              dv[s] = in ? (&S.sDy[u][0][0])[8 * p + 4 * s + q] : 0.0;
+            }
+#pragma unroll
+            for (int mt = 0; mt < IT; ++mt) {
+              if (mt < nti) {
+#pragma unroll
+                for (int nt = 0; nt < IT; ++nt) {
+                  if (nt < nti) {
+                    mma(Pr[mt][nt], gt[mt][0], gt[nt][0]);
+                    mma(Pr[mt][nt], gt[mt][1], gt[nt][1]);
+                  }
+                }
+                mma(Wt[mt], dv[0], gt[mt][0]);
+                mma(Wt[mt], dv[1], gt[mt][1]);
+              }
+            }
+            continue;
+          }
           // ---- blocked Sherman-Morrison over rows [0, te) of tile u (solver.py:297-304) ----
           const bool inb = p < te;
           double gm[IT][2];
@@ -999,13 +1047,21 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
         if (end) break;
         bar_arrive_n(BAR_EMPTY, PANEL_THREADS);
       }
-      // P^-1 to global, W for the x contraction
+      // P^-1 to global (deferred fold: Q to the scratch for the inversion), W (B^T dy) for
+      // the x contraction
+      r = rh;  // (the projection warps counted the panel phase's growth themselves)
+      double* Qs = &S.sG[0][0][0][0] + R * 8;
 #pragma unroll
       for (int mt = 0; mt < IT; ++mt) {
 #pragma unroll
-        for (int nt = 0; nt < IT; ++nt)
-          *reinterpret_cast<double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q) =
-              make_double2(Pr[mt][nt][0], Pr[mt][nt][1]);
+        for (int nt = 0; nt < IT; ++nt) {
+          if (defer)
+            *reinterpret_cast<double2*>(Qs + (8 * mt + p) * R + 8 * nt + 2 * q) =
+                make_double2(Pr[mt][nt][0], Pr[mt][nt][1]);
+          else
+            *reinterpret_cast<double2*>(Pg + (8 * mt + p) * R + 8 * nt + 2 * q) =
+                make_double2(Pr[mt][nt][0], Pr[mt][nt][1]);
+        }
 #pragma unroll
         for (int e = 0; e < 2; ++e) Wsm[8 * mt + 2 * q + e][p] = Wt[mt][e];
       }
@@ -1013,6 +1069,95 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
     PPROBE(home ? 11 : 7);
     __syncthreads();
     PPROBE(home ? 12 : 12);
+
+    if (defer) {
+      // ---- P^-1 = Q^-1 (in-place Gauss-Jordan, Q is SPD with pivots >= 1: no pivoting),
+      // the certificate, W = P^-1 (B^T dy).  Thread (ti, tj) keeps Q[ti][tj + TPR jj] in
+      // registers; step kk publishes pivot row and column through a two-deep buffer (one
+      // CTA barrier per step).  Rows / columns past the rank are zero and stay zero.
+      constexpr int TPR = PANEL_THREADS / R, NC = R / TPR;
+      static_assert(offsetof(SMT, bulkpad) + sizeof(S.bulkpad) - offsetof(SMT, sG) >=
+                        sizeof(double) * (R * 8 + R * R),
+                    "deferred fold: Q fits the scratch");
+      double* Qs = &S.sG[0][0][0][0] + R * 8;
+      const int tid = threadIdx.x, ti = tid / TPR, tj = tid % TPR;
+      double a[NC], fq = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) {
+        a[jj] = Qs[ti * R + tj + TPR * jj];
+        fq = fma(a[jj], a[jj], fq);
+      }
+      __syncthreads();  // Q is in registers: the scratch past W is free
+      double* rowk = Qs;           // [2][R]
+      double* colk = Qs + 2 * R;   // [2][R]
+      double* red = Qs + 4 * R;    // [2][4]
+#pragma unroll 1
+      for (int kk = 0; kk < r; ++kk) {
+        double* rk = rowk + (kk & 1) * R;
+        double* ck = colk + (kk & 1) * R;
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          const int j = tj + TPR * jj;
+          if (ti == kk) rk[j] = a[jj];
+          if (j == kk) ck[ti] = a[jj];
+        }
+        __syncthreads();
+        const double pv = rcp64(rk[kk]);
+        const double f = ck[ti] * pv;
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          const int j = tj + TPR * jj;
+          const double rv = rk[j];
+          if (ti == kk) a[jj] = (j == kk) ? pv : rv * pv;
+          else a[jj] = (j == kk) ? -f : fma(-f, rv, a[jj]);
+        }
+      }
+      double fp = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) fp = fma(a[jj], a[jj], fp);
+      fq = warp_sum(fq);
+      fp = warp_sum(fp);
+      __syncthreads();  // the last step's buffers are read
+      if (lane == 0) {
+        red[w] = fq;
+        red[4 + w] = fp;
+      }
+      __syncthreads();
+      const double kq = (red[0] + red[1]) + (red[2] + red[3]);
+      const double kp = (red[4] + red[5]) + (red[6] + red[7]);
+      constexpr double DEFER_KAPPA = 1e6;
+      if (!(kq * kp <= DEFER_KAPPA * DEFER_KAPPA)) {  // (a NaN fails too)
+        redo = true;
+#ifdef RGB_PANEL_PROBE
+        if (tid == 0) atomicAdd(&g_pprobe[31], 1ull);
+#endif
+        continue;
+      }
+      PPROBE(24);
+      // W = P^-1 (B^T dy): partial sums over the own columns, reduced over the row's threads
+      double wv[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wv[c] = 0.0;
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) {
+        const int j = tj + TPR * jj;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) wv[c] = fma(a[jj], Wsm[j][c], wv[c]);
+        Pg[ti * R + j] = a[jj];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+#pragma unroll
+        for (int o = 1; o < TPR; o <<= 1) wv[c] += __shfl_xor_sync(FULL, wv[c], o);
+      }
+      __syncthreads();  // B^T dy is read
+      if (tj == 0) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Wsm[ti][c] = wv[c];
+      }
+      __syncthreads();
+      PPROBE(25);
+    }
 
     // ---- write back; x = x0 + C~^T W on the own columns ------------------------------
     if (!home) {
@@ -1071,6 +1216,9 @@ static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows
                           const void* targets, int64_t tg_stride, int64_t T, const rgb_logs& logs,
                           cudaStream_t stream, int num_sms) {
   auto kern = blk::panel_kernel<R, M, TI>;
+  // RGB_PANEL_SEQ=1: the sequential Sherman-Morrison chain for every stream (A/B runs, tests)
+  const char* seq_env = getenv("RGB_PANEL_SEQ");
+  const int seq_only = (seq_env && seq_env[0] && seq_env[0] != '0') ? 1 : 0;
   const size_t smem = sizeof(blk::PanelSmem<R, M, TI>);
   static bool attr[64] = {};
   smem_attr_once(kern, smem, attr);
@@ -1089,7 +1237,7 @@ static int launch_panel_t(const rgb_config& cfg, rgb_state& st, const void* rows
   }
   kern<<<(unsigned)grid, blk::PANEL_THREADS, smem, stream>>>(cfg, st, (const TI*)rows, rows_stride,
                                                              (const TI*)targets, tg_stride, T, logs.branch,
-                                                             (double*)logs.coords, (unsigned*)ws);
+                                                             (double*)logs.coords, (unsigned*)ws, seq_only);
   const cudaError_t e = cudaGetLastError();
   if (ws) cudaFreeAsync(ws, stream);
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;

@@ -32,7 +32,7 @@ lib.rgb_panel_probe(buf.ctypes.data, 0)
 print("ms", e0.elapsed_time(e1))
 names = {0: "P setup", 1: "P row mode", 2: "P stage wait", 3: "P projection", 4: "P proj barrier",
          5: "P wait EMPTY", 6: "P growth", 7: "P end", 8: "H setup", 9: "H wait FULL", 10: "H scan",
-         11: "H end", 12: "end sync wait", 13: "x+writeback+sync", 16: " bulk: warp-0 solve", 17: " bulk: barrier", 18: " bulk: C~ update", 19: " bulk: new rows", 20: " bulk: between tiles", 21: " scan: pre-LDL", 22: " scan: LDL", 23: " scan: post-LDL"}
+         11: "H end", 12: "end sync wait", 13: "x+writeback+sync", 16: " bulk: warp-0 solve", 17: " bulk: barrier", 18: " bulk: C~ update", 19: " bulk: new rows", 20: " bulk: between tiles", 21: " scan: pre-LDL", 22: " scan: LDL", 23: " scan: post-LDL", 24: "defer: invert", 25: "defer: W", 31: "defer: redo count x4096"}
 ws = np.zeros(8192, np.uint32)
 lib.rgb_panel_wslot.argtypes = [ctypes.c_void_p]
 lib.rgb_panel_wslot(ws.ctypes.data)

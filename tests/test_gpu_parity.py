@@ -309,6 +309,40 @@ def test_c3_kernels_against_oracle_and_each_other(kernel, monkeypatch):
         assert relerr(other["x"][i], res["x"][i]) <= 1e-10
 
 
+def test_panel_deferred_fold_and_sequential_fallback(monkeypatch):
+    """The panel kernel folds a fresh stream's dependent rows in deferred form
+    (Q = B^T B and B^T dy accumulated on the tensor cores, one inversion at the
+    end) when kappa_F(Q) <= 1e6 and falls back to the sequential Sherman-Morrison
+    chain otherwise; RGB_PANEL_SEQ=1 forces the chain for every stream.  384
+    full-length config-3 streams hold both kinds (~5 % are past the bound): both
+    modes against the oracle (branches, ranks, x, P^-1) and against each other."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch("c3", list(range(384)))
+    out = {}
+    res = run_batched(rows, tg, r_cap=32)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=32, out=out)
+    assert amb <= 4 and worst <= 2e-10
+    Q = np.einsum("bti,btj->bij", out["coords"], out["coords"])
+    ok = matched(res["branch"], res["nobs"], res["status"], out)
+    kap = np.array([np.linalg.norm(Q[b][:r, :r]) * np.linalg.norm(out["P"][b][:r, :r])
+                    for b, r in enumerate(out["rank"])])
+    assert (kap[ok] > 2e6).sum() >= 4 and (kap[ok] < 5e5).sum() >= 300  # both paths ran
+    P = res["solver"].gram_t.cpu().numpy()
+    for b in np.nonzero(ok)[0]:
+        assert relerr(P[b], out["P"][b]) <= (1e-9 if kap[b] < 5e5 else 1e-7), (b, kap[b])
+    monkeypatch.setenv("RGB_PANEL_SEQ", "1")
+    seq = run_batched(rows, tg, r_cap=32)
+    amb2, worst2 = compare_to_oracle(rows, tg, seq, r_cap=32)
+    assert amb2 <= 4 and worst2 <= 2e-10
+    assert np.array_equal(seq["branch"], res["branch"]) and np.array_equal(seq["rank"], res["rank"])
+    assert max(relerr(seq["x"][b], res["x"][b]) for b in range(rows.shape[0])) <= 2e-10
+    # streams past the bound took the chain in both runs: bitwise the same state
+    Ps = seq["solver"].gram_t.cpu().numpy()
+    far = np.nonzero(ok & (kap > 2e6))[0]
+    assert all(np.array_equal(Ps[b], P[b]) and np.array_equal(seq["x"][b], res["x"][b]) for b in far)
+
+
 def test_c5_short_streams_ill_conditioned_start():
     """256-row prefixes: the first dependent tiles see the least-conditioned
     8x8 systems (large coordinates on a fresh 16-row basis)."""
