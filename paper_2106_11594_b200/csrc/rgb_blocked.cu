@@ -68,6 +68,52 @@ struct WarpSmem {
   static_assert(sizeof(Cs) + sizeof(At) >= sizeof(double) * R * (M + 2), "staging");
 };
 
+// In-place Gauss-Jordan inverse of the SPD matrix A (fragment layout A[mt][nt][e] =
+// A[8mt+p][8nt+2q+e], pivots >= 1: no pivoting); rows / columns past the rank r are zero
+// and stay zero.  Returns |A|_F^2 |A^-1|_F^2.  Not inlined: it runs once or twice per
+// stream, and its 8 IT unrolled steps would otherwise sit in the tile loop's code.
+template <int IT>
+__device__ __noinline__ double gj_invert(double (&A)[IT][IT][2], int r, int p, int q) {
+  double fq = 0.0, fp = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt) fq = fma(A[mt][nt][0], A[mt][nt][0], fma(A[mt][nt][1], A[mt][nt][1], fq));
+#pragma unroll
+  for (int kk = 0; kk < 8 * IT; ++kk) {
+    if (kk < r) {  // (uniform)
+      const int mk = kk >> 3, pk = kk & 7, qk = (kk & 7) >> 1, ek = kk & 1;
+      const double pv = rcp64(__shfl_sync(FULL, A[mk][mk][ek], 4 * pk + qk));
+      double rowv[IT][2], f[IT];
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt) {
+        rowv[nt][0] = __shfl_sync(FULL, A[mk][nt][0], 4 * pk + q);
+        rowv[nt][1] = __shfl_sync(FULL, A[mk][nt][1], 4 * pk + q);
+      }
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt) f[mt] = __shfl_sync(FULL, A[mt][mk][ek], 4 * p + qk) * pv;
+#pragma unroll
+      for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ir = (mt == mk) && (p == pk);
+            const bool jc = (nt == mk) && (2 * q + e == (kk & 7));
+            double v = fma(-f[mt], rowv[nt][e], A[mt][nt][e]);
+            if (ir) v = rowv[nt][e] * pv;
+            if (jc) v = ir ? pv : -f[mt];
+            A[mt][nt][e] = v;
+          }
+    }
+  }
+#pragma unroll
+  for (int mt = 0; mt < IT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < IT; ++nt) fp = fma(A[mt][nt][0], A[mt][nt][0], fma(A[mt][nt][1], A[mt][nt][1], fp));
+  return warp_sum(fq) * warp_sum(fp);
+}
+
 #ifndef RGB_BLOCKED_MINB
 #define RGB_BLOCKED_MINB 3
 #endif
@@ -80,17 +126,30 @@ template <int M, int R, int KC, int WARPS, bool GEN, typename TI, bool KM = fals
 __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     rgb_config cfg, rgb_state st, const TI* __restrict__ rows, int64_t rstride,
     const TI* __restrict__ tgts, int64_t tstride, int64_t T, uint8_t* __restrict__ blog,
-    double* __restrict__ clog, int seq_only) {
+    double* __restrict__ clog, int seq_only, unsigned* __restrict__ next_stream) {
   static_assert(M % 8 == 0 && R % 8 == 0 && KC == 8, "shape");
   constexpr int JT = M / 8, JK = M / 4, IT = R / 8, IK = R / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = lane >> 2, q = lane & 3;
   WarpSmem<M, R, KC, TI>& S = reinterpret_cast<WarpSmem<M, R, KC, TI>*>(smem_raw)[wid];
-  const int64_t nwarps = (int64_t)gridDim.x * WARPS;
 
+  // Streams are claimed dynamically, one atomicAdd per warp and stream (a stream whose deferred
+  // fold is folded again costs twice the others: a static round robin left the busiest warp
+  // ~10 % behind the mean); without a counter every warp has at most one stream.
   bool redo = false;  // the deferred fold of the stream failed its conditioning certificate
-  for (int64_t b = (int64_t)blockIdx.x * WARPS + wid; b < cfg.num_streams; b += nwarps) {
+  int64_t b = (int64_t)blockIdx.x * WARPS + wid;
+  for (unsigned iter = 0;; ++iter) {
+    if (!redo) {
+      if (next_stream) {
+        unsigned c = 0;
+        if (lane == 0) c = atomicAdd(next_stream, 1u);
+        b = __shfl_sync(FULL, c, 0);
+      } else if (iter > 0) {
+        break;
+      }
+    }
+    if (b >= cfg.num_streams) break;
     const bool seq = redo || seq_only != 0;
     redo = false;
     int status = st.status[b];
@@ -156,6 +215,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     }
     const bool has_x0 = __any_sync(FULL, nz);
     __syncwarp();
+    double esq = eps_sq<double>(cfg, r);  // the rank test's threshold, refreshed when the rank grows
 
     // ---- tile loop -----------------------------------------------------------------
     // front(i): coords, rejections and the rank test of tile i (tensor cores);
@@ -205,28 +265,24 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       F.dyx[0] = yy.x;
       F.dyx[1] = yy.y;
       // row norms |a_t|^2 (solver.py:267)
+      // (R = A - G C accumulates onto the tile itself: C is stored negated)
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int nt = 0; nt < JT; ++nt) {
         const double2 v = slot(As, nt * 32);
+        X.acc[nt][0] = v.x;
+        X.acc[nt][1] = v.y;
         s4[(2 * nt) & 3] = fma(v.x, v.x, s4[(2 * nt) & 3]);
         s4[(2 * nt + 1) & 3] = fma(v.y, v.y, s4[(2 * nt + 1) & 3]);
       }
       F.asq = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) F.g[nt][0] = F.g[nt][1] = X.g2[nt][0] = X.g2[nt][1] = 0.0;
-      // R = A - G C accumulates onto the tile itself (C is stored negated)
-#pragma unroll
-      for (int jt = 0; jt < JT; ++jt) {
-        const double2 v = slot(As, jt * 32);
-        X.acc[jt][0] = v.x;
-        X.acc[jt][1] = v.y;
-      }
     };
     // G = A C~^T (M = t, N = i, K = j; solver.py:286): K steps 2J, 2J + 1
     // (hi = false: rank <= 8, rows 8.. of C~ are zero and N tile 1 is skipped)
     auto front_g1 = [&](int s, int J, Front& F, FrontAcc& X, bool hi = true) {
-      const double2 v = slot(&S.At[s][0][lane][0], J * 32);
+      const double2 v = make_double2(X.acc[J][0], X.acc[J][1]);  // (the tile: R has not started)
 #pragma unroll
       for (int nt = 0; nt < IT; ++nt) {
         if (nt > 0 && !hi) break;
@@ -273,7 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       const unsigned yb1 = __ballot_sync(FULL, !isfinite(F.dyx[1]));
       const bool ybad = (((p & 1) ? yb1 : yb0) & (0x11111111u << (p >> 1))) != 0u;
       const bool valid = p >= row_start && p < F.tv;
-      const bool dep = is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r));
+      const bool dep = is_dependent<double>(rsq, asq, esq);
       const bool bad = !isfinite(asq) || ybad;
       const unsigned stopm = __ballot_sync(FULL, q == 0 && valid && (!dep || bad));
       F.badm = __ballot_sync(FULL, q == 0 && valid && bad);
@@ -486,15 +542,13 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         dv[s] = in ? ((q & 1) ? y1 : y0) : 0.0;
       }
 #pragma unroll
-      for (int mt = 0; mt < IT; ++mt) {
+      for (int s = 0; s < 2; ++s)  // (s outermost: no two consecutive MMAs on one accumulator)
 #pragma unroll
-        for (int nt = 0; nt < IT; ++nt) {
-          mma(Pr[mt][nt], gt[mt][0], gt[nt][0]);
-          mma(Pr[mt][nt], gt[mt][1], gt[nt][1]);
+        for (int mt = 0; mt < IT; ++mt) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) mma(Pr[mt][nt], gt[mt][s], gt[nt][s]);
+          mma(Wt[mt], dv[s], gt[mt][s]);
         }
-        mma(Wt[mt], dv[0], gt[mt][0]);
-        mma(Wt[mt], dv[1], gt[mt][1]);
-      }
     };
     auto accum_front = [&](const Front& F, int64_t tile_n, int s_n, Front& N) {
       FrontAcc A;
@@ -506,59 +560,40 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       for (int kt = 0; kt < IK; ++kt) front_g2(kt, N, A);
       front_end(s_n, 0, N, A);
     };
-    // P^-1 = Q^-1 in place in the fragment registers (Gauss-Jordan; Q is SPD with pivots
-    // >= 1, so no pivoting), then W = P^-1 (B^T dy).  Returns |Q|_F^2 |Q^-1|_F^2.
-    auto invert_q = [&]() -> double {
-      double fq = 0.0, fp = 0.0;
+    // P^-1 = Q^-1 (gj_invert on a copy, so that Pr stays in registers), then
+    // W = P^-1 (B^T dy).  Returns |Q|_F^2 |Q^-1|_F^2.
+    auto invert_q = [&](bool apply) -> double {
+      double Tq[IT][IT][2];
 #pragma unroll
       for (int mt = 0; mt < IT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < IT; ++nt) fq = fma(Pr[mt][nt][0], Pr[mt][nt][0], fma(Pr[mt][nt][1], Pr[mt][nt][1], fq));
+        for (int nt = 0; nt < IT; ++nt) {
+          Tq[mt][nt][0] = Pr[mt][nt][0];
+          Tq[mt][nt][1] = Pr[mt][nt][1];
+        }
+      const double kap2 = gj_invert<IT>(Tq, r, p, q);
+      if (apply) {
 #pragma unroll
-      for (int kk = 0; kk < R; ++kk) {
-        if (kk < r) {  // (uniform; rows / columns past the rank are zero and stay zero)
-          const int mk = kk >> 3, pk = kk & 7, qk = (kk & 7) >> 1, ek = kk & 1;
-          const double pv = rcp64(__shfl_sync(FULL, Pr[mk][mk][ek], 4 * pk + qk));
-          double rowv[IT][2], f[IT];
+        for (int mt = 0; mt < IT; ++mt)
 #pragma unroll
           for (int nt = 0; nt < IT; ++nt) {
-            rowv[nt][0] = __shfl_sync(FULL, Pr[mk][nt][0], 4 * pk + q);
-            rowv[nt][1] = __shfl_sync(FULL, Pr[mk][nt][1], 4 * pk + q);
+            Pr[mt][nt][0] = Tq[mt][nt][0];
+            Pr[mt][nt][1] = Tq[mt][nt][1];
           }
+        double wn[IT][2];
 #pragma unroll
-          for (int mt = 0; mt < IT; ++mt) f[mt] = __shfl_sync(FULL, Pr[mt][mk][ek], 4 * p + qk) * pv;
+        for (int nt = 0; nt < IT; ++nt) {
+          wn[nt][0] = wn[nt][1] = 0.0;
 #pragma unroll
-          for (int mt = 0; mt < IT; ++mt)
+          for (int kt = 0; kt < IK; ++kt) mma(wn[nt], Wt[kt >> 1][kt & 1], Pr[nt][kt >> 1][kt & 1]);
+        }
 #pragma unroll
-            for (int nt = 0; nt < IT; ++nt)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const bool ir = (mt == mk) && (p == pk);
-                const bool jc = (nt == mk) && (2 * q + e == (kk & 7));
-                double v = fma(-f[mt], rowv[nt][e], Pr[mt][nt][e]);
-                if (ir) v = rowv[nt][e] * pv;
-                if (jc) v = ir ? pv : -f[mt];
-                Pr[mt][nt][e] = v;
-              }
+        for (int nt = 0; nt < IT; ++nt) {
+          Wt[nt][0] = wn[nt][0];
+          Wt[nt][1] = wn[nt][1];
         }
       }
-#pragma unroll
-      for (int mt = 0; mt < IT; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < IT; ++nt) fp = fma(Pr[mt][nt][0], Pr[mt][nt][0], fma(Pr[mt][nt][1], Pr[mt][nt][1], fp));
-      double wn[IT][2];
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt) {
-        wn[nt][0] = wn[nt][1] = 0.0;
-#pragma unroll
-        for (int kt = 0; kt < IK; ++kt) mma(wn[nt], Wt[kt >> 1][kt & 1], Pr[nt][kt >> 1][kt & 1]);
-      }
-#pragma unroll
-      for (int nt = 0; nt < IT; ++nt) {
-        Wt[nt][0] = wn[nt][0];
-        Wt[nt][1] = wn[nt][1];
-      }
-      return warp_sum(fq) * warp_sum(fp);
+      return kap2;
     };
 
     // logs of dependent rows [rs, te): branch 0 and the coordinate row gamma_t
@@ -706,6 +741,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       }
       __syncwarp();
       r += 1;
+      esq = eps_sq<double>(cfg, r);
     };
     auto grow = [&](const Front& F, int ts) {
       // W gains row r: y - a.x0 of row ts (x = x0 + C~^T W stays exact)
@@ -798,7 +834,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
             project_row(s, ts, rsq, asq);
             const double yv = (double)S.Yt[s][4 * p + (ts >> 1)][ts & 1];  // y[ts][c = p]
             const bool bad = !isfinite(asq) || __any_sync(FULL, !isfinite(yv));
-            if (bad || r >= R || is_dependent<double>(rsq, asq, eps_sq<double>(cfg, r))) break;
+            if (bad || r >= R || is_dependent<double>(rsq, asq, esq)) break;
             grow_core(yv, rsq, t0, ts);
           }
           if (ts < tv) {
@@ -816,8 +852,22 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         front_x0((int)(tile & 1), F);
       }
     }
+    // Deferred fold: R + 32 rows into the stream kappa_F(Q) already tells how the final one
+    // will turn out (on the config-5 workload: every stream that ends past DEFER_KAPPA is past
+    // half of it here, 0.3 % of the others are too), so a stream that will not pass starts
+    // over with the sequential chain now instead of after its last row.  (A heuristic only:
+    // the certificate at the end decides.)
+    constexpr int64_t CK_TILE = (R + 32) / TT;
+    constexpr double DEFER_KAPPA = 1e6;
+    bool give_up = false;
     for (; tile < ntiles; ++tile) {
       const int s = (int)(tile & 1);
+      if (defer && tile == CK_TILE && ntiles > 4 * CK_TILE) {
+        if (!(invert_q(false) <= 0.25 * DEFER_KAPPA * DEFER_KAPPA)) {
+          give_up = true;
+          break;
+        }
+      }
       if (F.tstar >= F.tv && first_row == 0) {
         // every row of the tile is dependent: scan(i) overlaps front(i+1)
         prefetch(tile + 2, s);
@@ -869,10 +919,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     cp_wait<0>();
     __syncwarp();
     if (defer) {
-      constexpr double DEFER_KAPPA = 1e6;
-      if (!(invert_q() <= DEFER_KAPPA * DEFER_KAPPA)) {  // (a NaN fails too)
+      if (give_up || !(invert_q(true) <= DEFER_KAPPA * DEFER_KAPPA)) {  // (a NaN fails too)
         redo = true;  // nothing is written yet: the same stream again, sequentially
-        b -= nwarps;
         continue;
       }
     }
@@ -926,6 +974,8 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
 
 }  // namespace blk
 
+cudaMemPool_t workspace_pool();  // rgb_grid.cu
+
 namespace {
 constexpr int BM = 64, BR = 16, BK = 8;
 #ifndef RGB_BLOCKED_WARPS
@@ -960,9 +1010,19 @@ static int launch_blocked_t(const rgb_config& cfg, rgb_state& st, const TI* rows
   // RGB_BLOCKED_SEQ=1: the sequential Sherman-Morrison chain for every stream (A/B runs, tests)
   const char* seq_env = getenv("RGB_BLOCKED_SEQ");
   const int seq_only = (seq_env && seq_env[0] && seq_env[0] != '0') ? 1 : 0;
+  // the stream counter: 4 bytes, stream-ordered, from the library's device pool (not needed
+  // when every warp gets at most one stream)
+  void* ws = nullptr;
+  if (cfg.num_streams > grid * BWARPS) {
+    cudaMemPool_t pool = workspace_pool();
+    if (!pool || cudaMallocFromPoolAsync(&ws, 256, pool, stream) != cudaSuccess) return RGB_E_CUDA;
+    cudaMemsetAsync(ws, 0, sizeof(unsigned), stream);
+  }
   kern<<<(unsigned)grid, BWARPS * 32, smem, stream>>>(cfg, st, rows, rows_stride, targets, tg_stride, T,
-                                                      logs.branch, (double*)logs.coords, seq_only);
-  return cudaGetLastError() == cudaSuccess ? RGB_OK : RGB_E_CUDA;
+                                                      logs.branch, (double*)logs.coords, seq_only, (unsigned*)ws);
+  const cudaError_t e = cudaGetLastError();
+  if (ws) cudaFreeAsync(ws, stream);
+  return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 
 int launch_blocked(const rgb_config& cfg, rgb_state& st, const void* rows, int64_t rows_stride,
