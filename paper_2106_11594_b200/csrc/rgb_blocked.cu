@@ -1,7 +1,7 @@
 // rgb_blocked.cu -- batched rank-Greville update on fp64 tensor cores (sm_100a).
 //
-// One warp owns one stream at a time (persistent grid, static round-robin over
-// streams) and consumes its rows in tiles of 8.  Inside a run of dependent
+// One warp owns one stream at a time (persistent grid, streams claimed dynamically)
+// and consumes its rows in tiles of 8.  Inside a run of dependent
 // rows the basis C and dual C~ do not change (solver.py:297-304 touch only
 // P^-1 and x), so the per-row GEMVs of the reference become 8-row contractions
 // on DMMA.8x8x4 (mma.sync m8n8k4 f64), with every reduction inside the tensor
@@ -24,6 +24,12 @@
 // row appends W's row r = y - a.x0 (exact algebra for x' = x + K dy with
 // C~' = [C~ - gamma K^T; K^T]), and x is materialised once at the end of the
 // call.  dy0 = y - a.x0 - gamma^T W is the reference's a-priori residual.
+//
+// Deferred fold (general variant, a fresh stream): the chain above is the recursive form
+// of P^-1 = (B^T B)^-1, W = P^-1 B^T dy, and neither the rank test nor growth reads
+// P^-1 or W -- so the tiles only accumulate Q = B^T B and B^T dy (12 MMAs, no chain) and
+// Q is inverted once per call, accepted when kappa_F(Q) <= 1e6; a stream that fails is
+// folded again with the chain (see `defer` below and DESIGN.md).  18.96 -> 16.36 ms.
 //
 // Independent rows (solver.py:305-318, _grow solver.py:368-397) split the tile:
 // the dependent prefix is folded, the row grows the basis (K = rej/|rej|^2,

@@ -28,6 +28,11 @@
 //    arrive, home syncs; EMPTY: home arrives, projection warps sync).  In the
 //    general variant growth never reads P^-1 or W (W's new row is y - a.x0,
 //    P^-1 = diag(P^-1, 1)), so a growth row only appends a marker to the slot.
+//  * Deferred fold: for a fresh stream the home warp only accumulates Q = B^T B and
+//    B^T dy from the slot (no dependent chain) and the CTA inverts Q once at the end,
+//    accepted when kappa_F(Q) <= 1e6; otherwise the stream is folded again with the
+//    chain above (see the comment at `defer` below and DESIGN.md).  Config 3:
+//    2.18 -> 1.93 ms.
 //  * A fresh stream's leading independent rows are taken one at a time on the
 //    CUDA cores (all four warps split the columns), as in the warp-group
 //    kernel's row mode; W's rows of that phase go to the home warp through

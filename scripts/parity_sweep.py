@@ -22,8 +22,11 @@ from paper_2106_11594_b200.batched import BatchedSolver  # noqa: E402
 
 
 def sweep(cfg_name, B, kernel="default"):
-    """kernel: "default" (the dispatcher's choice) or "warp-group" (RGB_NO_PANEL=1)."""
+    """kernel: "default" (the dispatcher's choice: deferred fold with the sequential
+    chain as its fallback), "sequential" (RGB_BLOCKED_SEQ / RGB_PANEL_SEQ: the chain
+    for every stream) or "warp-group" (RGB_NO_PANEL=1)."""
     os.environ["RGB_NO_PANEL"] = "1" if kernel == "warp-group" else "0"
+    os.environ["RGB_BLOCKED_SEQ"] = os.environ["RGB_PANEL_SEQ"] = "1" if kernel == "sequential" else "0"
     c = workloads.CONFIGS[cfg_name]
     rows_d, tg_d = workloads.device_batch(cfg_name, 0, B, "cuda")
     n = rows_d.shape[1]
@@ -43,7 +46,9 @@ def sweep(cfg_name, B, kernel="default"):
     X, XO = bs.solution.cpu().numpy(), oracle.solution(o)
     err = np.abs(X - XO).max(axis=(1, 2)) / np.maximum(1.0, np.abs(XO).max(axis=(1, 2)))
     dep_rho = np.where(o["branch"] == 0, o["rho"], 0.0).max(axis=1)
-    return {"config": cfg_name, "kernel": {"c5": "one-warp", "c3": "panel"}[cfg_name] if kernel == "default" else kernel,
+    name = {"c5": "one-warp", "c3": "panel"}[cfg_name]
+    return {"config": cfg_name,
+            "kernel": {"default": name + " (deferred fold)", "sequential": name + " (sequential chain)"}.get(kernel, kernel),
             "streams": B, "rows_per_stream": n, "band": list(BAND),
             "exact_branch_logs": cmp["exact"], "first_disagreement_in_band": cmp["band_disagree"],
             "first_disagreement_outside_band": cmp["outside_disagree"],
@@ -52,12 +57,14 @@ def sweep(cfg_name, B, kernel="default"):
             "oracle_runaway": int((o["status"] != 0).sum()), "device_frozen": int((dev_status != 0).sum()),
             "x_checked": int(ok.sum()), "rank_mismatch_on_exact": int((rank[ok] != o["rank"][ok]).sum()),
             "x_relerr_max": float(err[ok].max()), "x_relerr_median": float(np.median(err[ok])),
+            "x_relerr_q999": float(np.quantile(err[ok], 0.999)),
             "max_dependent_rho_quantiles": {q: float(np.quantile(dep_rho, float(q))) for q in
                                             ("0.5", "0.99", "0.999", "1.0")},
             "tolerance": 1e-9}
 
 
-out = [sweep("c5", 16384), sweep("c3", 4096), sweep("c3", 4096, "warp-group")]
+out = [sweep("c5", 16384), sweep("c5", 16384, "sequential"), sweep("c3", 4096), sweep("c3", 4096, "sequential"),
+       sweep("c3", 4096, "warp-group")]
 print(json.dumps(out, indent=1))
 path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "parity_sweep.json")
 json.dump(out, open(path, "w"), indent=1)

@@ -343,6 +343,82 @@ def test_panel_deferred_fold_and_sequential_fallback(monkeypatch):
     assert all(np.array_equal(Ps[b], P[b]) and np.array_equal(seq["x"][b], res["x"][b]) for b in far)
 
 
+def test_blocked_deferred_fold_and_sequential_fallback(monkeypatch):
+    """The one-warp config-5 kernel: the same deferred fold (Q and B^T dy accumulated per
+    tile, in-register Gauss-Jordan at the end, a first kappa check 48 rows in) with the
+    sequential chain as the fallback; RGB_BLOCKED_SEQ=1 forces the chain.  512 full-length
+    streams x 8 right-hand sides (the Gaussian half holds streams past the bound)."""
+    from paper_2106_11594_b200 import workloads
+
+    rows, tg = workloads.host_batch("c5", list(range(512)))
+    out = {}
+    res = run_batched(rows, tg, r_cap=16)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=16, out=out)
+    assert amb <= 4 and worst <= 2e-10
+    ok = matched(res["branch"], res["nobs"], res["status"], out)
+    Q = np.einsum("bti,btj->bij", out["coords"], out["coords"])
+    kap = np.array([np.linalg.norm(Q[b][:r, :r]) * np.linalg.norm(out["P"][b][:r, :r])
+                    for b, r in enumerate(out["rank"])])
+    assert (kap[ok] > 2e6).sum() >= 3 and (kap[ok] < 2.5e5).sum() >= 400  # both paths ran
+    P = res["solver"].gram_t.cpu().numpy()
+    for b in np.nonzero(ok)[0]:
+        assert relerr(P[b], out["P"][b]) <= (1e-9 if kap[b] < 2.5e5 else 1e-7), (b, kap[b])
+    monkeypatch.setenv("RGB_BLOCKED_SEQ", "1")
+    seq = run_batched(rows, tg, r_cap=16)
+    amb2, worst2 = compare_to_oracle(rows, tg, seq, r_cap=16)
+    assert amb2 <= 4 and worst2 <= 2e-10
+    assert np.array_equal(seq["branch"], res["branch"]) and np.array_equal(seq["rank"], res["rank"])
+    live = (res["status"] == 0)
+    assert max(relerr(seq["x"][b], res["x"][b]) for b in np.nonzero(live)[0]) <= 2e-10
+    Ps = seq["solver"].gram_t.cpu().numpy()
+    far = np.nonzero(ok & (kap > 2e6))[0]
+    assert all(np.array_equal(Ps[b], P[b]) and np.array_equal(seq["x"][b], res["x"][b]) for b in far)
+
+
+@pytest.mark.parametrize("m,r_cap,k,env", [(64, 16, 3, "RGB_BLOCKED_SEQ"), (128, 32, 1, "RGB_PANEL_SEQ"),
+                                          (256, 16, 2, "RGB_PANEL_SEQ")])
+def test_deferred_and_sequential_fold_agree_on_edge_cases(m, r_cap, k, env, monkeypatch):
+    """Deferred fold against the forced sequential chain (and the oracle) where the stream
+    does not simply run to its end: a NaN row mid-stream, a NaN target, a stream that
+    hits the rank capacity, all-zero rows, duplicated rows before the rank is reached
+    (dependent rows ahead of independent ones inside a tile), a short call (T = 5)."""
+    rng = np.random.default_rng(11)
+    T, r = 150, r_cap // 2
+
+    def lowrank():
+        return rng.standard_normal((T, r)) @ rng.standard_normal((r, m))
+
+    A = np.stack([lowrank() for _ in range(7)])
+    Y = rng.standard_normal((7, T, k))
+    A[1, 37, 5] = np.nan                       # non-finite row
+    Y[2, 61, k - 1] = np.inf                   # non-finite target
+    A[3] = rng.standard_normal((T, m))         # full rank: freezes at the capacity
+    A[4] = 0.0                                 # rank 0 throughout
+    A[5, 1:6] = A[5, 0]                        # duplicates before the rank is reached
+    A[5, 9] = 2.0 * A[5, 7] - A[5, 8]
+    for T_call in (T, 5):
+        rows, tg = A[:, :T_call], Y[:, :T_call]
+        res = run_batched(rows, tg, r_cap=r_cap)
+        monkeypatch.setenv(env, "1")
+        seq = run_batched(rows, tg, r_cap=r_cap)
+        monkeypatch.delenv(env)
+        for key in ("rank", "nobs", "status", "branch"):
+            assert np.array_equal(res[key], seq[key]), key
+        assert (res["status"][[1, 2]] == 2).all() and res["nobs"][1] == min(37, T_call)
+        if T_call == T:
+            assert res["status"][3] == 1 and res["rank"][3] == r_cap and res["rank"][4] == 0
+        for b in range(7):
+            assert relerr(res["x"][b], seq["x"][b]) <= 1e-10, b
+        P, Ps = res["solver"].gram_t.cpu().numpy(), seq["solver"].gram_t.cpu().numpy()
+        assert relerr(P, Ps) <= 1e-9
+        fin = [0, 3, 4, 5, 6]  # (the oracle, like the reference, has no non-finite path)
+        o = oracle.ingest(rows[fin], tg[fin], r_cap=r_cap)
+        assert np.array_equal(o["rank"], res["rank"][fin]) and np.array_equal(o["status"], res["status"][fin])
+        X = oracle.solution(o)
+        for i, b in enumerate(fin):
+            assert relerr(res["x"][b], X[i]) <= 1e-9, b
+
+
 def test_c5_short_streams_ill_conditioned_start():
     """256-row prefixes: the first dependent tiles see the least-conditioned
     8x8 systems (large coordinates on a fresh 16-row basis)."""
