@@ -556,10 +556,45 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           mma(Wt[mt], dv[s], gt[mt][s]);
         }
     };
+    // the same for a whole tile of dependent rows (the fast path): G^T through the warp's
+    // scratch rows instead of shuffles -- stored in the accumulator layout, read at
+    // 64 nt + 32 s + 8 q + p it is G[4s + q][8nt + p], conflict-free (no growth is pending on
+    // this path, so the scratch rows are free)
+    auto accum_tile = [&](const Front& F) {
+      double* sc = &S.u.ind.gam[0];
+      static_assert(sizeof(S.u.ind) >= sizeof(double) * TT * R, "G tile fits the scratch rows");
+#pragma unroll
+      for (int nt = 0; nt < IT; ++nt)
+        *reinterpret_cast<double2*>(sc + (nt * 32 + lane) * 2) = make_double2(F.g[nt][0], F.g[nt][1]);
+      __syncwarp();
+      double gt[IT][2], dv[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const bool in = 4 * s + q < F.tv;
+#pragma unroll
+        for (int nt = 0; nt < IT; ++nt) {
+          const double v = sc[64 * nt + 32 * s + 8 * q + p];
+          gt[nt][s] = in ? v : 0.0;
+        }
+        const int srcy = 4 * p + 2 * s + (q >> 1);
+        const double y0 = __shfl_sync(FULL, F.dyx[0], srcy);
+        const double y1 = __shfl_sync(FULL, F.dyx[1], srcy);
+        dv[s] = in ? ((q & 1) ? y1 : y0) : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int mt = 0; mt < IT; ++mt) {
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) mma(Pr[mt][nt], gt[mt][s], gt[nt][s]);
+          mma(Wt[mt], dv[s], gt[mt][s]);
+        }
+    };
     auto accum_front = [&](const Front& F, int64_t tile_n, int s_n, Front& N) {
       FrontAcc A;
       front_begin(tile_n, s_n, N, A);
-      accum(F, 0, F.tv);
+      accum_tile(F);
 #pragma unroll
       for (int J = 0; J < JK / 2; ++J) front_g1(s_n, J, N, A);
 #pragma unroll

@@ -404,15 +404,15 @@ def test_deferred_and_sequential_fold_agree_on_edge_cases(m, r_cap, k, env, monk
         monkeypatch.delenv(env)
         for key in ("rank", "nobs", "status", "branch"):
             assert np.array_equal(res[key], seq[key]), key
-        assert (res["status"][[1, 2]] == 2).all() and res["nobs"][1] == min(37, T_call)
         if T_call == T:
+            assert (res["status"][[1, 2]] == 2).all() and res["nobs"][1] == 37 and res["nobs"][2] == 61
             assert res["status"][3] == 1 and res["rank"][3] == r_cap and res["rank"][4] == 0
         for b in range(7):
             assert relerr(res["x"][b], seq["x"][b]) <= 1e-10, b
         P, Ps = res["solver"].gram_t.cpu().numpy(), seq["solver"].gram_t.cpu().numpy()
         assert relerr(P, Ps) <= 1e-9
         fin = [0, 3, 4, 5, 6]  # (the oracle, like the reference, has no non-finite path)
-        o = oracle.ingest(rows[fin], tg[fin], r_cap=r_cap)
+        o = oracle.ingest(np.ascontiguousarray(rows[fin]), np.ascontiguousarray(tg[fin]), r_cap=r_cap)
         assert np.array_equal(o["rank"], res["rank"][fin]) and np.array_equal(o["status"], res["status"][fin])
         X = oracle.solution(o)
         for i, b in enumerate(fin):
