@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
     // scratch rows instead of shuffles -- stored in the accumulator layout, read at
     // 64 nt + 32 s + 8 q + p it is G[4s + q][8nt + p], conflict-free (no growth is pending on
     // this path, so the scratch rows are free)
-    auto accum_tile = [&](const Front& F) {
+    auto accum_tile = [&](const Front& F, int st) {
       double* sc = &S.u.ind.gam[0];
       static_assert(sizeof(S.u.ind) >= sizeof(double) * TT * R, "G tile fits the scratch rows");
 #pragma unroll
@@ -576,10 +576,10 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           const double v = sc[64 * nt + 32 * s + 8 * q + p];
           gt[nt][s] = in ? v : 0.0;
         }
-        const int srcy = 4 * p + 2 * s + (q >> 1);
-        const double y0 = __shfl_sync(FULL, F.dyx[0], srcy);
-        const double y1 = __shfl_sync(FULL, F.dyx[1], srcy);
-        dv[s] = in ? ((q & 1) ? y1 : y0) : 0.0;
+        // dy = y here (x0 = 0); the stage stores y[t][c] at 8c + t: the same targets with the
+        // rows on q (read before the stage is handed to the next prefetch)
+        const double yv = (double)(&S.Yt[st][0][0])[8 * p + 4 * s + q];
+        dv[s] = in ? yv : 0.0;
       }
       __syncwarp();
 #pragma unroll
@@ -590,16 +590,6 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
           for (int nt = 0; nt < IT; ++nt) mma(Pr[mt][nt], gt[mt][s], gt[nt][s]);
           mma(Wt[mt], dv[s], gt[mt][s]);
         }
-    };
-    auto accum_front = [&](const Front& F, int64_t tile_n, int s_n, Front& N) {
-      FrontAcc A;
-      front_begin(tile_n, s_n, N, A);
-      accum_tile(F);
-#pragma unroll
-      for (int J = 0; J < JK / 2; ++J) front_g1(s_n, J, N, A);
-#pragma unroll
-      for (int kt = 0; kt < IK; ++kt) front_g2(kt, N, A);
-      front_end(s_n, 0, N, A);
     };
     // P^-1 = Q^-1 (gj_invert on a copy, so that Pr stays in registers), then
     // W = P^-1 (B^T dy).  Returns |Q|_F^2 |Q^-1|_F^2.
@@ -910,11 +900,13 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
         }
       }
       if (F.tstar >= F.tv && first_row == 0) {
-        // every row of the tile is dependent: scan(i) overlaps front(i+1)
+        // every row of the tile is dependent: scan(i) overlaps front(i+1); the deferred
+        // fold reads the tile's targets from its stage before the stage is refilled
+        if (defer) accum_tile(F, s);
         prefetch(tile + 2, s);
         cp_wait<1>();
         Front N;
-        if (defer) accum_front(F, tile + 1, s ^ 1, N);
+        if (defer) front(tile + 1, s ^ 1, 0, N);
         else scan_front(F, tile + 1, s ^ 1, N);
         log_dependent(F, 0, F.tv);
         front_x0(s ^ 1, N);
