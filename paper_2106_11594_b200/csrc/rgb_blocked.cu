@@ -902,12 +902,21 @@ __global__ void __launch_bounds__(WARPS * 32, RGB_BLOCKED_MINB) blocked_kernel(
       if (F.tstar >= F.tv && first_row == 0) {
         // every row of the tile is dependent: scan(i) overlaps front(i+1); the deferred
         // fold reads the tile's targets from its stage before the stage is refilled
-        if (defer) accum_tile(F, s);
+        if (defer) {
+          // (the tile's front is dead once it is folded and logged: the next one goes
+          // straight into F)
+          accum_tile(F, s);
+          log_dependent(F, 0, F.tv);
+          consumed = F.t0 + F.tv;
+          prefetch(tile + 2, s);
+          cp_wait<1>();
+          front(tile + 1, s ^ 1, 0, F);
+          continue;
+        }
         prefetch(tile + 2, s);
         cp_wait<1>();
         Front N;
-        if (defer) front(tile + 1, s ^ 1, 0, N);
-        else scan_front(F, tile + 1, s ^ 1, N);
+        scan_front(F, tile + 1, s ^ 1, N);
         log_dependent(F, 0, F.tv);
         front_x0(s ^ 1, N);
         consumed = F.t0 + F.tv;
