@@ -296,13 +296,14 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
 #pragma unroll
             for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = h[nt][0] = h[nt][1] = 0.0;
 #pragma unroll
-            for (int ks = 0; ks < KS / 2; ++ks)
+            for (int nt = 0; nt < IT; ++nt)  // (rank tile outermost: one guard per tile, as in gcoords below)
+              if (nt < nti) {
 #pragma unroll
-              for (int nt = 0; nt < IT; ++nt)
-                if (nt < nti) {
+                for (int ks = 0; ks < KS / 2; ++ks) {
                   mma(g[nt], acc[ks >> 1][ks & 1], S.Df[nt][ks][lane]);
                   mma(h[nt], acc[(ks + KS / 2) >> 1][ks & 1], S.Df[nt][ks + KS / 2][lane]);
                 }
+              }
 #pragma unroll
             for (int nt = 0; nt < IT; ++nt) {
               g[nt][0] += h[nt][0];
@@ -629,11 +630,13 @@ __global__ void __launch_bounds__(PANEL_THREADS, (M <= 128 ? 3 : 1)) panel_kerne
         double h[IT][2];
 #pragma unroll
         for (int nt = 0; nt < IT; ++nt) g[nt][0] = g[nt][1] = h[nt][0] = h[nt][1] = 0.0;
+        // rank tile outermost: one guard per tile instead of one per MMA pair (the guards are
+        // branches with a WARPSYNC each); two chains keep the DMMA pipe's issue interval
 #pragma unroll
-        for (int ks = 0; ks < KS / 2; ++ks) {
+        for (int nt = 0; nt < IT; ++nt) {
+          if (nt < nti) {
 #pragma unroll
-          for (int nt = 0; nt < IT; ++nt) {
-            if (nt < nti) {
+            for (int ks = 0; ks < KS / 2; ++ks) {
               mma(g[nt], acc[ks >> 1][ks & 1], S.Df[nt][ks][lane]);
               mma(h[nt], acc[(ks + KS / 2) >> 1][ks & 1], S.Df[nt][ks + KS / 2][lane]);
             }
