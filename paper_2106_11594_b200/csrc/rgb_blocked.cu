@@ -29,7 +29,7 @@
 // of P^-1 = (B^T B)^-1, W = P^-1 B^T dy, and neither the rank test nor growth reads
 // P^-1 or W -- so the tiles only accumulate Q = B^T B and B^T dy (12 MMAs, no chain) and
 // Q is inverted once per call, accepted when kappa_F(Q) <= 1e6; a stream that fails is
-// folded again with the chain (see `defer` below and DESIGN.md).  18.96 -> 14.92 ms.
+// folded again with the chain (see `defer` below and DESIGN.md).  18.96 -> 14.24 ms.
 //
 // Independent rows (solver.py:305-318, _grow solver.py:368-397) split the tile:
 // the dependent prefix is folded, the row grows the basis (K = rej/|rej|^2,

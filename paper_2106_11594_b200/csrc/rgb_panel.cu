@@ -32,7 +32,7 @@
 //    B^T dy from the slot (no dependent chain) and the CTA inverts Q once at the end,
 //    accepted when kappa_F(Q) <= 1e6; otherwise the stream is folded again with the
 //    chain above (see the comment at `defer` below and DESIGN.md).  Config 3:
-//    2.18 -> 1.93 ms.
+//    2.18 -> 1.95 ms, 1.75 ms with the projection's G loop rank-tile-outermost.
 //  * A fresh stream's leading independent rows are taken one at a time on the
 //    CUDA cores (all four warps split the columns), as in the warp-group
 //    kernel's row mode; W's rows of that phase go to the home warp through
