@@ -33,6 +33,8 @@
 // where the column CTAs read W to form x = x0 + C~^T W.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "rgb_mma.cuh"
 
 namespace cg = cooperative_groups;
@@ -149,7 +151,7 @@ template <int R, int TT, int CW, bool GEN, typename TI>
 __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_state st, const TI* __restrict__ rows,
                                                         int64_t rstride, const TI* __restrict__ tgts, int64_t tstride,
                                                         int64_t T, uint8_t* __restrict__ blog,
-                                                        double* __restrict__ clog) {
+    double* __restrict__ clog, int seq_only) {
   constexpr int IT = R / 8, IK = R / 4, NXT = (R + 8) / 8, GX = R + 8, MT = TT / 8;
   constexpr int NG = NW / MT;                       // warps per M tile
   constexpr int NJ1 = (NXT + NG - 1) / NG;          // P1 N tiles per warp
@@ -194,10 +196,21 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
     nsync += 1;
   };
 
+  bool redo = false;  // the stream's deferred fold failed its conditioning certificate
   for (int64_t b = cid; b < cfg.num_streams; b += ncid) {
+    const bool seq = redo || seq_only != 0;
+    redo = false;
     int status = st.status[b];
     if (status) continue;  // uniform across the cluster
     int r = st.rank[b];
+    // Deferred fold (general variant, a fresh stream; rgb_blocked.cu has the derivation): the
+    // home CTA only accumulates Q = B^T B and B^T dy from each projection's G -- no LDL^T
+    // chain, no barrier inside a block -- and inverts Q once at the end of the call; the
+    // result is accepted when kappa_F(Q) <= 1e6, otherwise the whole cluster folds the
+    // stream again with the sequential chain (a fresh stream's factors are never read, so
+    // the column CTAs' early write-back of C~ and C does not matter).
+    const bool fresh = (r == 0);
+    const bool defer = GEN && fresh && !seq;
     const int64_t nobs0 = st.nobs[b];
     const int rc = cfg.r_cap;  // stored capacity (<= R): global row stride; rows past it are zero
     double* Cg = reinterpret_cast<double*>(st.basis) + b * (int64_t)rc * M;
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         const int i = 8 * nt + (l >> 2), col = c0 + 4 * kt + (l & 3);
         double v = 0.0;
         if (col < M) {
-          if (i < rc) v = Dg[(int64_t)i * M + col];
+          if (i < rc) v = fresh ? 0.0 : Dg[(int64_t)i * M + col];
           else if (i >= R && i - R < k) v = Xg[(int64_t)(i - R) * M + col];
         }
         C.Ds[nt][kt][l] = v;
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         const int l = e & 31, nt = (e >> 5) % (CW / 8), kt = e / (32 * (CW / 8));
         const int col = c0 + 8 * nt + (l >> 2);
         const int i = 4 * kt + (l & 3);
-        C.Cs[kt][nt][l] = (col < M && i < rc) ? -Cg[(int64_t)i * M + col] : 0.0;
+        C.Cs[kt][nt][l] = (col < M && i < rc && !fresh) ? -Cg[(int64_t)i * M + col] : 0.0;
       }
       auto prefetch = [&](int64_t pan, int s) {
         if (pan < npan) {
@@ -452,7 +465,8 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         if (col < M && i < rc) Cg[(int64_t)i * M + col] = -C.Cs[kt][nt][l];
       }
       cluster_sync_all();  // home has folded every projection: W is final
-      {
+      redo = defer && rem(ncol)->u.home.flags[2] != 0;  // (the same value in every CTA)
+      if (!redo) {
         SM* h = rem(ncol);
         for (int e = tid; e < R * 8; e += NT) C.Wl[e >> 3][e & 7] = h->u.home.Wb[e >> 3][e & 7];
         __syncthreads();
@@ -463,7 +477,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
           if (c0 + jl < M) Xg[(int64_t)cc * M + c0 + jl] = x;
         }
       }
-      if (c == 0 && tid == 0) {
+      if (!redo && c == 0 && tid == 0) {
         st.rank[b] = r;
         st.nobs[b] = nobs0 + consumed;
         st.status[b] = status;
@@ -474,7 +488,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       auto& H = S.u.home;
       for (int e = tid; e < R * R; e += NT) {
         const int i = e / R, i2 = e % R;
-        H.Ps[i][i2] = (i < rc && i2 < rc) ? Pg[(int64_t)i * rc + i2] : 0.0;
+        H.Ps[i][i2] = (i < rc && i2 < rc && !fresh) ? Pg[(int64_t)i * rc + i2] : 0.0;
       }
       for (int e = tid; e < R * 8; e += NT) H.Wb[e >> 3][e & 7] = 0.0;
       auto prefetch = [&](int64_t pan, int s) {
@@ -492,7 +506,55 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
       // panel row base (M = I + G P G^T = L D L^T, E = L^-1; Y = P G^T E^T;
       // P -= Y D^-1 Y^T; W += Y D^-1 E dy0, dy0 = y - a.x0 - G W)
       unsigned nblk = 0;  // dependent blocks folded (selects the U buffer)
+      auto dep_log = [&](const double (*Gs)[HGS], int base, int rs, int te, int64_t t0) {
+        if (tid < 8 && base + tid >= rs && base + tid < te) {  // logs of the dependent rows
+          const int64_t row = b * T + t0 + base + tid;
+          if (blog) blog[row] = 0;
+          if (clog)
+            for (int i = 0; i < rc; ++i) clog[row * rc + i] = Gs[base + tid][i];
+        }
+      };
+      // deferred fold of rows [rs, te) of the block at panel row base: warp w owns rows
+      // 8w..8w+7 of Q (in Ps) and of B^T dy (in Wb); A = G^T (M = i, K = t), B = G (K = t,
+      // N = i') or dy (N = cc), both straight from the slot; no barrier
+      auto dep_block_deferred = [&](int s, const double (*Gs)[HGS], int base, int rs, int te, int64_t t0) {
+        if (8 * w < r) {
+          double a[2];
+#pragma unroll
+          for (int kt = 0; kt < 2; ++kt) {
+            const int t = base + 4 * kt + q;
+            a[kt] = (t >= rs && t < te) ? Gs[t][8 * w + p] : 0.0;
+          }
+#pragma unroll
+          for (int nt = 0; nt < IT; ++nt) {
+            if (8 * nt < r) {
+              const double2 v = *reinterpret_cast<const double2*>(&H.Ps[8 * w + p][8 * nt + 2 * q]);
+              double acc[2] = {v.x, v.y};
+#pragma unroll
+              for (int kt = 0; kt < 2; ++kt) {
+                const int t = base + 4 * kt + q;
+                mma(acc, a[kt], (t >= rs && t < te) ? Gs[t][8 * nt + p] : 0.0);
+              }
+              *reinterpret_cast<double2*>(&H.Ps[8 * w + p][8 * nt + 2 * q]) = make_double2(acc[0], acc[1]);
+            }
+          }
+          double wb[2] = {H.Wb[8 * w + p][2 * q], H.Wb[8 * w + p][2 * q + 1]};
+#pragma unroll
+          for (int kt = 0; kt < 2; ++kt) {
+            const int t = base + 4 * kt + q;
+            const double dy = (t >= rs && t < te) ? (double)H.Yv[s][t][p] - Gs[t][R + p] : 0.0;
+            mma(wb, a[kt], dy);
+          }
+          H.Wb[8 * w + p][2 * q] = wb[0];
+          H.Wb[8 * w + p][2 * q + 1] = wb[1];
+        }
+        dep_log(Gs, base, rs, te, t0);
+      };
       auto dep_block = [&](int s, const double (*Gs)[HGS], int base, int rs, int te, int64_t t0) {
+        if (defer) {
+          dep_block_deferred(s, Gs, base, rs, te, t0);
+          return;
+        }
         const int ub = (int)(nblk++ & 1u);
         const int kr = (r + 3) >> 2;  // K steps over the rank (rows beyond it are zero)
         const bool in_t = base + p >= rs && base + p < te;
@@ -620,12 +682,7 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
               *reinterpret_cast<double2*>(&H.Ps[8 * w + p][8 * nt + 2 * q]) = make_double2(acc[nt][0], acc[nt][1]);
         }
         PROBE(12);
-        if (tid < 8 && base + tid >= rs && base + tid < te) {  // logs of the dependent rows
-          const int64_t row = b * T + t0 + base + tid;
-          if (blog) blog[row] = 0;
-          if (clog)
-            for (int i = 0; i < rc; ++i) clog[row * rc + i] = Gs[base + tid][i];
-        }
+        dep_log(Gs, base, rs, te, t0);
         // no barrier: the next block reads only its own rows of P^-1 and W, writes
         // the other U buffer, and its first barrier orders the rest
         PROBE(13);
@@ -740,10 +797,78 @@ __global__ void __launch_bounds__(NT, 1) cluster_kernel(rgb_config cfg, rgb_stat
         if (!stopped) consumed = t0 + tv;
       }
       blk::cp_wait<0>();
-      for (int e = tid; e < rc * rc; e += NT) Pg[e] = H.Ps[e / rc][e % rc];
+      __syncthreads();
+      if (defer) {
+        // P^-1 = Q^-1 in place (Gauss-Jordan, Q is SPD with pivots >= 1: no pivoting; the
+        // pivot row and column of a step go through the U buffers), the certificate
+        // kappa_F(Q) = |Q|_F |Q^-1|_F <= 1e6, then W = P^-1 (B^T dy)
+        double* rowk = &H.Ub[0][0][0];
+        double* colk = rowk + R;
+        double* red = colk + R;  // [2][NW]
+        double fq = 0.0, fp = 0.0;
+        for (int e = tid; e < r * r; e += NT) {
+          const double v = H.Ps[e / r][e % r];
+          fq = fma(v, v, fq);
+        }
+#pragma unroll 1
+        for (int kk = 0; kk < r; ++kk) {
+          if (tid < r) {
+            rowk[tid] = H.Ps[kk][tid];
+            colk[tid] = H.Ps[tid][kk];
+          }
+          __syncthreads();
+          const double pv = blk::rcp64(rowk[kk]);
+          for (int e = tid; e < r * r; e += NT) {
+            const int i = e / r, j = e % r;
+            const double f = colk[i] * pv, rv = rowk[j];
+            double v = fma(-f, rv, H.Ps[i][j]);
+            if (i == kk) v = rv * pv;
+            if (j == kk) v = (i == kk) ? pv : -f;
+            H.Ps[i][j] = v;
+          }
+          __syncthreads();
+        }
+        for (int e = tid; e < r * r; e += NT) {
+          const double v = H.Ps[e / r][e % r];
+          fp = fma(v, v, fp);
+        }
+        fq = warp_sum(fq);
+        fp = warp_sum(fp);
+        if (lane == 0) {
+          red[w] = fq;
+          red[NW + w] = fp;
+        }
+        __syncthreads();
+        double kq = 0.0, kp = 0.0;
+        for (int u = 0; u < NW; ++u) {
+          kq += red[u];
+          kp += red[NW + u];
+        }
+        const bool bad = !(kq * kp <= 1e12);  // (a NaN fails too)
+        if (tid == 0) H.flags[2] = bad ? 1 : 0;
+        redo = bad;
+        if (!bad) {
+          double wv = 0.0;
+          const int i = tid >> 3, cc = tid & 7;  // NT = 8 R at most: one (i, cc) per thread and pass
+          for (int i0 = 0; i0 < R; i0 += NT / 8) {
+            wv = 0.0;
+            if (i0 + i < r)
+              for (int j = 0; j < r; ++j) wv = fma(H.Ps[i0 + i][j], H.Wb[j][cc], wv);
+            rowk[(i0 + i) * 8 + cc] = wv;  // (R * 8 doubles: the U buffers hold 2 R * 8)
+          }
+          __syncthreads();
+          for (int e = tid; e < R * 8; e += NT) H.Wb[e >> 3][e & 7] = (e >> 3) < r ? rowk[e] : 0.0;
+          __syncthreads();
+        }
+      } else if (tid == 0) {
+        H.flags[2] = 0;
+      }
+      if (!redo)
+        for (int e = tid; e < rc * rc; e += NT) Pg[e] = H.Ps[e / rc][e % rc];
       cluster_sync_all();  // W final for the column CTAs
       cluster_sync_all();  // they have read it
     }
+    if (redo) b -= ncid;  // nothing of the state's rank / counters / x is written: the same stream again
   }
 }
 
@@ -783,8 +908,11 @@ static int launch_cluster_t(const rgb_config& cfg, rgb_state& st, const void* ro
   lc.gridDim = dim3((unsigned)(ncl * nclusters));
   const TI* rp = (const TI*)rows;
   const TI* tp = (const TI*)targets;
+  // RGB_CLUSTER_SEQ=1: the sequential Sherman-Morrison chain for every stream (A/B runs, tests)
+  const char* seq_env = getenv("RGB_CLUSTER_SEQ");
+  const int seq_only = (seq_env && seq_env[0] && seq_env[0] != '0') ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, cfg, st, rp, rows_stride, tp, tg_stride, T, logs.branch,
-                                     (double*)logs.coords);
+                                     (double*)logs.coords, seq_only);
   return e == cudaSuccess ? RGB_OK : RGB_E_CUDA;
 }
 

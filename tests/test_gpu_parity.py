@@ -1020,6 +1020,42 @@ def test_runs_are_bitwise_deterministic(cfg, r_cap, streams, n):
     assert np.array_equal(a["solver"].gram_t.cpu().numpy(), b["solver"].gram_t.cpu().numpy())
 
 
+def test_cluster_kernel_deferred_fold_and_fallback(monkeypatch):
+    """The cluster kernel's home CTA defers the fold of a fresh general-variant stream too
+    (Q and B^T dy accumulated per block, one inversion per call, kappa_F <= 1e6), and the
+    whole cluster folds the stream again with the chain otherwise; RGB_CLUSTER_SEQ=1 forces
+    the chain.  Streams 0-2 are well conditioned; the dependent rows of streams 3-5 are 300
+    times longer along one basis direction (kappa_F past 5e6, the rank decisions unaffected)."""
+    rng = np.random.default_rng(23)
+    B, n, m, r = 6, 260, 512, 12
+    rows = np.zeros((B, n, m))
+    for b in range(B):
+        G1, G2 = rng.standard_normal((n, r)), rng.standard_normal((r, m))
+        if b >= 3:
+            G1[r:, 0] *= 3e2
+        rows[b] = G1 @ G2
+    tg = rng.standard_normal((B, n, 2))
+    out = {}
+    res = run_batched(rows, tg, r_cap=64)
+    amb, worst = compare_to_oracle(rows, tg, res, r_cap=64, out=out)
+    assert amb == 0 and worst <= 1e-9
+    Q = np.einsum("bti,btj->bij", out["coords"], out["coords"])
+    kap = np.array([np.linalg.norm(Q[b][:r_, :r_]) * np.linalg.norm(out["P"][b][:r_, :r_])
+                    for b, r_ in enumerate(out["rank"])])
+    assert (kap[:3] < 2e5).all() and (kap[3:] > 5e6).all(), kap
+    P = res["solver"].gram_t.cpu().numpy()
+    for b in range(B):
+        assert relerr(P[b], out["P"][b]) <= (1e-9 if b < 3 else 1e-6), (b, kap[b])
+    monkeypatch.setenv("RGB_CLUSTER_SEQ", "1")
+    seq = run_batched(rows, tg, r_cap=64)
+    assert np.array_equal(seq["branch"], res["branch"]) and np.array_equal(seq["rank"], res["rank"])
+    Ps = seq["solver"].gram_t.cpu().numpy()
+    for b in range(B):
+        assert relerr(seq["x"][b], res["x"][b]) <= 1e-10
+        if b >= 3:  # past the bound: the chain in both runs, bitwise the same state
+            assert np.array_equal(Ps[b], P[b]) and np.array_equal(seq["x"][b], res["x"][b])
+
+
 def test_cluster_kernel_more_streams_than_clusters():
     """20 streams of m = 1024 on 16-CTA clusters (at most ~9 resident): each
     cluster folds several streams in turn, its mbarrier phases and ring slots
