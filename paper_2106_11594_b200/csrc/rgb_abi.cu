@@ -5,8 +5,9 @@
 // match wins: the one-warp tensor-core kernel (m 64, r_cap 16, k <= 8), the
 // panel kernel (general variant: m 128 with r_cap 16 / 32, m 256 with r_cap 16;
 // RGB_NO_PANEL=1 in the environment turns it off, for A/B runs and tests;
-// RGB_BLOCKED_SEQ=1 / RGB_PANEL_SEQ=1 make these two kernels fold every stream with
-// the sequential chain instead of the deferred fold, see rgb_blocked.cu), the
+// RGB_BLOCKED_SEQ=1 / RGB_PANEL_SEQ=1 / RGB_CLUSTER_SEQ=1 make these kernels and the cluster
+// kernel fold every stream with the sequential chain instead of the deferred fold, see
+// rgb_blocked.cu), the
 // warp-group kernel (m 128 / 256 with r_cap 16 / 32, every variant), the cluster kernel
 // (r_cap 64, m <= 1 080) and the grid kernel (a few large streams, m <= 2 368,
 // r_cap <= 512) -- the last two for calls of 8+ rows -- and the shape-generic

@@ -31,6 +31,12 @@
 // runs concurrently with the next panels' projections instead of stalling
 // them; the hardware cluster barrier is used only at the end of a stream,
 // where the column CTAs read W to form x = x0 + C~^T W.
+//
+// Deferred fold (general variant, a fresh stream): home only accumulates Q = B^T B and
+// B^T dy per block (no LDL^T, no barrier inside a block) and inverts Q once at the end,
+// accepted when kappa_F(Q) <= 1e6; otherwise the whole cluster folds the stream again with
+// the chain (rgb_blocked.cu has the derivation; RGB_CLUSTER_SEQ=1 forces the chain).
+// Config 2: 2.01 -> 1.78 ms.
 #include <cooperative_groups.h>
 
 #include <cstdlib>
