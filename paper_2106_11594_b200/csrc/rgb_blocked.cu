@@ -29,7 +29,7 @@
 // of P^-1 = (B^T B)^-1, W = P^-1 B^T dy, and neither the rank test nor growth reads
 // P^-1 or W -- so the tiles only accumulate Q = B^T B and B^T dy (12 MMAs, no chain) and
 // Q is inverted once per call, accepted when kappa_F(Q) <= 1e6; a stream that fails is
-// folded again with the chain (see `defer` below and DESIGN.md).  18.96 -> 14.24 ms.
+// folded again with the chain (see `defer` below and DESIGN.md).  18.96 -> 14.15 ms.
 //
 // Independent rows (solver.py:305-318, _grow solver.py:368-397) split the tile:
 // the dependent prefix is folded, the row grows the basis (K = rej/|rej|^2,
@@ -121,7 +121,7 @@ __device__ __noinline__ double gj_invert(double (&A)[IT][IT][2], int r, int p, i
 }
 
 #ifndef RGB_BLOCKED_MINB
-#define RGB_BLOCKED_MINB 3
+#define RGB_BLOCKED_MINB 6  // x 2 warps: 12 warps per SM (same-box A/B: 4 x 3 +0.8 %, 12 x 1 +2.6 %, 1 x 12 +2.0 %)
 #endif
 
 // GEN: general variant only (the headline instantiation); !GEN: orthogonal /
@@ -1021,7 +1021,7 @@ cudaMemPool_t workspace_pool();  // rgb_grid.cu
 namespace {
 constexpr int BM = 64, BR = 16, BK = 8;
 #ifndef RGB_BLOCKED_WARPS
-#define RGB_BLOCKED_WARPS 4
+#define RGB_BLOCKED_WARPS 2
 #endif
 constexpr int BWARPS = RGB_BLOCKED_WARPS;
 }  // namespace
